@@ -1,0 +1,143 @@
+/*
+ * rbns.h — C ABI of the B200-native batched online solver for the velocity-only reduced Navier–Stokes
+ * method (arXiv 1807.11866).  Plain pointers and sizes only; no torch or CUDA C++ types in signatures.
+ *
+ * The reference ships no code for this path; its interface exists as the SPEC `online`
+ * module.  Each entry point names the SPEC operation it replaces:
+ *
+ *   rbns_model_create        <- ReducedModel hand-off to the online stage
+ *   rbns_solve               <- online.solve_block, batched ("batch sweep API")
+ *   rbns_solve_host          <- same, host buffers in/out (the query API a CPU caller binds)
+ *   rbns_reduced_operator    <- online.reduced_operator (residual + Jacobian)
+ *   rbns_recover_pressure    <- solve_block step 2, B_sp p = f_s - A_sv u
+ *   rbns_error_string        <- errors.RbflowError messages (reference errors.py:4-21)
+ *
+ * All arrays are IEEE fp64 (or the stated integer type), row-major, C-contiguous.  "dev" pointers are CUDA
+ * device pointers on the model's device; "host" pointers are ordinary (pinned or pageable) host memory.
+ * Per-sample outcomes are status codes, not errors (NON_CONVERGED is "a reportable outcome,
+ * not a crash").  Every function returns RBNS_OK (0) or a nonzero rbns_error; rbns_last_error_message()
+ * gives the detail for the calling thread.
+ */
+#ifndef RBNS_H_
+#define RBNS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBNS_ABI_VERSION 1
+#define RBNS_MAX_TERMS 16
+
+/* θ_q(μ) descriptor kinds; μ = (alpha [rad], Re).  value = scale * base. */
+enum rbns_theta_kind {
+  RBNS_THETA_CONST = 0,       /* 1                           */
+  RBNS_THETA_COS_K = 1,       /* cos(k alpha)                */
+  RBNS_THETA_SIN_K = 2,       /* sin(k alpha)                */
+  RBNS_THETA_COS_SIN_POW = 3, /* cos(alpha)^k * sin(alpha)^m */
+  RBNS_THETA_MONOMIAL = 4     /* alpha^k * Re^m  (the paper's scale*phi^k*u_inf^m) */
+};
+
+/* per-sample outcome (int8) */
+enum rbns_status {
+  RBNS_CONVERGED = 0,         /* ||delta||_2 <= tol * ||u||_2                         */
+  RBNS_NON_CONVERGED = 1,     /* hit max_iter                           */
+  RBNS_SINGULAR_SYSTEM = 2,   /* zero / non-finite pivot in the Newton system         */
+  RBNS_SINGULAR_RECOVERY = 3, /* pressure Gramian B_sp not SPD          */
+  RBNS_NONFINITE = 4          /* Newton update produced inf/nan; u keeps last iterate */
+};
+
+enum rbns_error {
+  RBNS_OK = 0,
+  RBNS_ERR_INVALID_ARGUMENT = 1,
+  RBNS_ERR_CUDA = 2,
+  RBNS_ERR_OUT_OF_MEMORY = 3,
+  RBNS_ERR_UNSUPPORTED = 4,
+  RBNS_ERR_NO_PRESSURE = 5
+};
+
+typedef struct rbns_theta_term {
+  int32_t kind;
+  int32_t k;
+  int32_t m;
+  int32_t reserved;
+  double scale;
+} rbns_theta_term;
+
+typedef struct rbns_model_desc {
+  int32_t n;                    /* reduced velocity dimension N (paper M_V)              */
+  int32_t q;                    /* affine terms Q, 1..RBNS_MAX_TERMS                      */
+  int32_t n_p;                  /* pressure dimension Np (0 = no recovery operators)      */
+  int32_t reserved;
+  const double* A;              /* host Q x N x N      projected a-terms (times nu online)  */
+  const double* C;              /* host Q x N x N x N  C[q][j][k][l] = c_q(u_j, u_k, u_l)   */
+  const double* f;              /* host Q x N          projected loads                      */
+  const double* Mp;             /* host Np x Np SPD pressure Gramian (B_sp) or NULL         */
+  const double* Bq;             /* host Q x Np x N coupling terms or NULL                   */
+  const rbns_theta_term* theta; /* host, Q descriptors                                      */
+} rbns_model_desc;
+
+typedef struct rbns_model rbns_model;
+
+/* Per-call statistics of the last rbns_solve / rbns_solve_host on this model (thread-unsafe read). */
+typedef struct rbns_stats {
+  int64_t sample_iterations;      /* sum over samples of Newton iterations performed               */
+  int64_t contraction_iterations; /* sample-iterations that ran the convective GEMM (iter >= 2)    */
+  int32_t newton_rounds;          /* outer iterations executed (max over samples)                  */
+  int32_t kernel_launches;        /* CUDA kernels launched by the call                             */
+  int32_t gemm_launches;          /* launches of the DMMA contraction kernel                       */
+  int32_t lu_launches;            /* launches of the Newton-update (Gauss-Jordan) kernel           */
+  double ms_gemm;                 /* device time (CUDA events) in the contraction kernel          */
+  double ms_lu;                   /* device time in the Newton-update kernel                      */
+  double ms_recovery;             /* device time in pressure recovery                             */
+  double ms_total;                /* device time of the whole call (excluding host copies)        */
+} rbns_stats;
+
+/* Copy operators to `device`, build the symmetrised GEMM operand S_q = C_q + C_q^(12),
+ * and factor Mp once.  The handle is immutable afterwards and may be shared by concurrent solves. */
+int rbns_model_create(const rbns_model_desc* desc, int device, rbns_model** out);
+int rbns_model_destroy(rbns_model* model);
+int rbns_model_info(const rbns_model* model, int32_t* n, int32_t* q, int32_t* n_p, int32_t* device);
+/* bytes of device memory the handle owns */
+int64_t rbns_model_device_bytes(const rbns_model* model);
+
+/* Batched velocity-only Newton solve + optional pressure recovery, device buffers.
+ *   mu          dev  B x 2   (alpha [rad], Re)
+ *   u           dev  B x N   out: velocity coefficients (last iterate)
+ *   p           dev  B x Np  out: recovered pressure, or NULL to skip recovery
+ *   iters       dev  B int32 out: Newton linear solves performed, incl. the accepted one
+ *   status      dev  B int8  out: rbns_status
+ *   last_update dev  B       out: ||delta||_2 of the last accepted update (NaN if none)
+ *   stream      cudaStream_t (NULL = legacy default stream)
+ * Blocks the host until the results are complete on `stream`.  Newton: u0 = 0, stop when
+ * ||delta||_2 <= tol * ||u_new||_2, at most max_iter solves. */
+int rbns_solve(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter,
+               double* u, double* p, int32_t* iters, int8_t* status, double* last_update, void* stream);
+
+/* Same as rbns_solve with HOST buffers: the call copies mu in and results out (the end-to-end path a
+ * CPU-side caller binds; host<->device copies are part of the call). */
+int rbns_solve_host(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter,
+                    double* u, double* p, int32_t* iters, int8_t* status, double* last_update,
+                    void* stream);
+
+/* Residual and Jacobian of the reduced system at states eta, batched (debug / FD tests).
+ *   mu dev B x 2, eta dev B x N, residual dev B x N, jacobian dev B x N x N (row l, column m = dR_l/du_m) */
+int rbns_reduced_operator(rbns_model* model, const double* mu, const double* eta, int64_t batch,
+                          double* residual, double* jacobian, void* stream);
+
+/* Pressure recovery alone for given velocities: p = Mp^{-1} sum_q theta_q(mu) B_q u (device buffers).
+ * status (dev, may be NULL) receives RBNS_SINGULAR_RECOVERY where Mp could not be factored. */
+int rbns_recover_pressure(rbns_model* model, const double* mu, const double* u, int64_t batch,
+                          double* p, int8_t* status, void* stream);
+
+int rbns_get_stats(const rbns_model* model, rbns_stats* out);
+
+const char* rbns_error_string(int code);
+const char* rbns_last_error_message(void);
+int rbns_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBNS_H_ */

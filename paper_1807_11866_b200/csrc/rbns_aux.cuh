@@ -1,0 +1,189 @@
+// rbns_aux.cuh — setup and bookkeeping kernels: GEMM-operand construction, active-set compaction (K5),
+// pressure recovery triangular solves (K4), reduced-operator readout.
+#pragma once
+
+#include "rbns_common.cuh"
+
+namespace rbns {
+
+// S[r][κ] for the contraction GEMM (layout documented in rbns_contract.cuh).  One-time, at model create.
+__global__ void build_velocity_operator(double* __restrict__ S, int64_t rows, int kalloc,
+                                        const double* __restrict__ C, const double* __restrict__ A, int N,
+                                        int Ne, int Q) {
+  const int64_t total = rows * kalloc;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / kalloc;
+    const int kap = int(idx - r * kalloc);
+    double v = 0.0;
+    const int64_t nn = int64_t(N) * N;
+    if (r < nn) {
+      const int l = int(r / N), m = int(r - int64_t(l) * N);
+      if (kap < Q * Ne) {
+        const int q = kap / Ne, k = kap - q * Ne;
+        if (k < N) {
+          const int64_t base = int64_t(q) * N * nn;
+          v = C[base + (int64_t(m) * N + k) * N + l] + C[base + (int64_t(k) * N + m) * N + l];
+        }
+      } else if (kap < Q * Ne + Q) {
+        const int q = kap - Q * Ne;
+        v = A[(int64_t(q) * N + l) * N + m];
+      }
+    } else if (r < nn + N) {
+      const int l = int(r - nn);
+      if (kap < Q * Ne) {
+        const int q = kap / Ne, k = kap - q * Ne;
+        if (k < N) v = A[(int64_t(q) * N + l) * N + k];
+      }
+    }
+    S[idx] = v;
+  }
+}
+
+// Sp[i][κ] = B_q[i][k] for κ = q·Ne + k: the recovery right-hand side Σ_q θ_q B_q u is the same GEMM.
+__global__ void build_pressure_operator(double* __restrict__ S, int np, int kalloc, const double* __restrict__ Bq,
+                                        int N, int Ne, int Q) {
+  const int64_t total = int64_t(np) * kalloc;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(idx / kalloc);
+    const int kap = int(idx - int64_t(i) * kalloc);
+    double v = 0.0;
+    if (kap < Q * Ne) {
+      const int q = kap / Ne, k = kap - q * Ne;
+      if (k < N) v = Bq[(int64_t(q) * np + i) * N + k];
+    }
+    S[idx] = v;
+  }
+}
+
+__global__ void init_solve(int32_t* act, int8_t* status, int32_t* iters, double* last, int64_t B) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B; i += int64_t(gridDim.x) * blockDim.x) {
+    act[i] = int32_t(i);
+    status[i] = int8_t(kStatusActive);
+    iters[i] = 0;
+    last[i] = __longlong_as_double(0x7ff8000000000000ULL);
+  }
+}
+
+__global__ void finalize_solve(int8_t* status, int64_t B) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B; i += int64_t(gridDim.x) * blockDim.x)
+    if (status[i] == int8_t(kStatusActive)) status[i] = int8_t(RBNS_NON_CONVERGED);
+}
+
+// K5: stable compaction of the still-active samples (deterministic order).  One CTA of 1024 threads.
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) compact_active(const int32_t* __restrict__ act_in, int32_t n_in,
+                                                                   const int8_t* __restrict__ status,
+                                                                   int32_t* __restrict__ act_out,
+                                                                   int32_t* __restrict__ count) {
+  __shared__ int32_t scan[kCompactThreads];
+  const int tid = threadIdx.x;
+  const int per = (n_in + kCompactThreads - 1) / kCompactThreads;
+  const int beg = min(n_in, tid * per), end = min(n_in, beg + per);
+  int c = 0;
+  for (int i = beg; i < end; ++i) c += status[act_in[i]] == int8_t(kStatusActive);
+  scan[tid] = c;
+  __syncthreads();
+  for (int off = 1; off < kCompactThreads; off <<= 1) {
+    const int v = tid >= off ? scan[tid - off] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int pos = scan[tid] - c;
+  for (int i = beg; i < end; ++i) {
+    const int32_t id = act_in[i];
+    if (status[id] == int8_t(kStatusActive)) act_out[pos++] = id;
+  }
+  if (tid == kCompactThreads - 1) *count = scan[tid];
+}
+
+// K4 (second half): p = L^{-T} L^{-1} r per sample, one warp per sample, M_p = L Lᵀ factored once.
+// Lt is Lᵀ row-major (column j of L contiguous) for the forward sweep, L row-major for the backward sweep.
+template <int CP>
+__global__ void __launch_bounds__(256) pressure_trisolve(const double* __restrict__ rbuf, int64_t ldr, int32_t n,
+                                                        const double* __restrict__ L, const double* __restrict__ Lt,
+                                                        int np, int ok, double* __restrict__ p,
+                                                        int8_t* __restrict__ status, const int32_t* __restrict__ ids) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const int id = ids ? ids[warp] : warp;
+  double r[CP];
+#pragma unroll
+  for (int c = 0; c < CP; ++c) {
+    const int i = lane + 32 * c;
+    r[c] = i < np ? rbuf[int64_t(warp) * ldr + i] : 0.0;
+  }
+  if (!ok) {
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+      const int i = lane + 32 * c;
+      if (i < np) p[int64_t(id) * np + i] = __longlong_as_double(0x7ff8000000000000ULL);
+    }
+    if (lane == 0 && status && status[id] == RBNS_CONVERGED) status[id] = RBNS_SINGULAR_RECOVERY;
+    return;
+  }
+  // forward: L y = r (y overwrites r)
+  for (int j = 0; j < np; ++j) {
+    double rj = 0.0;
+#pragma unroll
+    for (int c = 0; c < CP; ++c)
+      if (c == (j >> 5)) rj = r[c];
+    rj = __shfl_sync(0xffffffffu, rj, j & 31);
+    const double yj = rj / __ldg(&Lt[int64_t(j) * np + j]);
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+      const int i = lane + 32 * c;
+      if (i == j) r[c] = yj;
+      else if (i > j && i < np) r[c] = fma(-__ldg(&Lt[int64_t(j) * np + i]), yj, r[c]);
+    }
+  }
+  // backward: Lᵀ x = y
+  for (int j = np - 1; j >= 0; --j) {
+    double rj = 0.0;
+#pragma unroll
+    for (int c = 0; c < CP; ++c)
+      if (c == (j >> 5)) rj = r[c];
+    rj = __shfl_sync(0xffffffffu, rj, j & 31);
+    const double xj = rj / __ldg(&L[int64_t(j) * np + j]);
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+      const int i = lane + 32 * c;
+      if (i == j) r[c] = xj;
+      else if (i < j) r[c] = fma(-__ldg(&L[int64_t(j) * np + i]), xj, r[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CP; ++c) {
+    const int i = lane + 32 * c;
+    if (i < np) p[int64_t(id) * np + i] = r[c];
+  }
+}
+
+// reduced_operator readout: R = ½ J η + ½ ν A(μ)η − f(μ), J copied out (debug / FD path).
+__global__ void operator_readout(const double* __restrict__ Y, int64_t ldy, int32_t n, const double* __restrict__ eta,
+                                 const double* __restrict__ mu, const double* __restrict__ f, int N, int Q,
+                                 ThetaDesc th, double* __restrict__ R, double* __restrict__ Jout) {
+  const int b = blockIdx.x;
+  if (b >= n) return;
+  __shared__ double ths[RBNS_MAX_TERMS];
+  __shared__ double nus;
+  if (threadIdx.x == 0) {
+    const double alpha = mu[2 * b], re = mu[2 * b + 1];
+    nus = 1.0 / re;
+    for (int q = 0; q < Q; ++q) ths[q] = eval_theta_term(th, q, alpha, re);
+  }
+  __syncthreads();
+  const double* Yb = Y + int64_t(b) * ldy;
+  for (int64_t e = threadIdx.x; e < int64_t(N) * N; e += blockDim.x) Jout[int64_t(b) * N * N + e] = Yb[e];
+  for (int l = threadIdx.x; l < N; l += blockDim.x) {
+    double ju = 0.0;
+    for (int m = 0; m < N; ++m) ju = fma(Yb[int64_t(l) * N + m], eta[int64_t(b) * N + m], ju);
+    double fl = 0.0;
+    for (int q = 0; q < Q; ++q) fl = fma(ths[q], f[q * N + l], fl);
+    R[int64_t(b) * N + l] = 0.5 * ju + 0.5 * nus * Yb[int64_t(N) * N + l] - fl;
+  }
+}
+
+}  // namespace rbns

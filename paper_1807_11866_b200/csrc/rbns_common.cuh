@@ -1,0 +1,105 @@
+// rbns_common.cuh — shared device helpers: θ evaluation, PTX wrappers (mbarrier, TMA, DMMA).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "rbns.h"
+
+namespace rbns {
+
+constexpr int kStatusActive = 127;  // internal: sample still iterating
+
+struct ThetaDesc {
+  int32_t q;
+  int32_t kind[RBNS_MAX_TERMS];
+  int32_t k[RBNS_MAX_TERMS];
+  int32_t m[RBNS_MAX_TERMS];
+  double scale[RBNS_MAX_TERMS];
+};
+
+__device__ __forceinline__ double ipow(double x, int n) {
+  double r = 1.0;
+  for (int i = 0; i < n; ++i) r = r * x;
+  return r;
+}
+
+// θ_q(μ) — same rule, term by term, as paper_1807_11866_b200/affine.py:evaluate_weights
+// (SPEC.md:360-368 evaluate_weights; SPEC.md:335-338 CoefficientDescriptor).
+__device__ __forceinline__ double eval_theta_term(const ThetaDesc& d, int q, double alpha, double re) {
+  double base;
+  switch (d.kind[q]) {
+    case RBNS_THETA_CONST: base = 1.0; break;
+    case RBNS_THETA_COS_K: base = cos(double(d.k[q]) * alpha); break;
+    case RBNS_THETA_SIN_K: base = sin(double(d.k[q]) * alpha); break;
+    case RBNS_THETA_COS_SIN_POW: base = ipow(cos(alpha), d.k[q]) * ipow(sin(alpha), d.m[q]); break;
+    default: base = ipow(alpha, d.k[q]) * ipow(re, d.m[q]); break;
+  }
+  return d.scale[q] * base;
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+
+// 2-D TMA tile load global -> shared, completion signalled on an mbarrier (transaction bytes).
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
+}
+
+// FP64 tensor-core MMA (lowers to DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) * B(4x8).
+// Thread (g = lane>>2, t = lane&3) supplies A[g][t], B[t][g]; holds D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+}  // namespace rbns

@@ -1,0 +1,220 @@
+// rbns_contract.cuh — K1+K2: θ-weighted affine assembly fused into the convective contraction, as one
+// FP64 tensor-core (DMMA) GEMM over the μ batch.
+//
+//   Y[b][r] = Σ_κ X[b][κ] · S[r][κ]
+//     rows r < N²       : r = l·N + m  -> Jacobian entry J[l][m] = ν A(μ)[l][m] + Σ_q θ_q Σ_k S_q[m,k,l] u_k
+//     rows N² ≤ r < N²+N: r = N² + l   -> h[l] = (A(μ) u)[l]                   (residual helper)
+//     cols κ = q·Ne + k  : X = θ_q(μ_b) · u_b[k]           S = S_q[m,k,l] = C_q[m,k,l] + C_q[k,m,l]
+//     cols κ = Q·Ne + q  : X = ν_b · θ_q(μ_b)              S = A_q[l][m]
+// (PAPER.md:797-805 affine sums; PAPER.md:821-844 tensor + Fréchet chain.)
+//
+// Dataflow (one CTA = BM samples × a range of BN-row tiles):
+//   * S (the μ-independent operand, 56 MB at N=100/Q=7) is streamed from L2 by TMA (cp.async.bulk.tensor,
+//     evict_last policy) through an mbarrier ring fed by one producer warp; a stage is 8 κ = two boxes of
+//     BN rows × 4 κ (32-byte rows: the B-fragment loads of a half-warp cover 128 contiguous bytes).
+//   * X is never materialised.  The GEMM is regrouped per affine term,
+//         Y[b][r] = Σ_q θ_q(μ_b) · ( Σ_k u_b[k] S_q[r][k] )  +  Σ_q ν_b θ_q(μ_b) A_q[r],
+//     so the A fragments are plain u values (resident smem tile, loaded once per CTA) and θ_q is applied
+//     once per term to a partial accumulator (32 DFMA per thread per term) — no per-fragment scaling on the
+//     FP64 pipe the DMMAs share.
+//   * 8 consumer warps each own a 32-sample × 32-row tile (4×4 DMMA.8x8x4 fragments, two accumulator sets).
+#pragma once
+
+#include <cuda.h>
+
+#include "rbns_common.cuh"
+
+namespace rbns {
+
+struct ContractParams {
+  const int32_t* act;     // sample ids of this chunk (length n); NULL = identity
+  int32_t n;              // samples in this chunk
+  const double* u;        // [B][N] states, indexed by sample id
+  const double* mu;       // [B][2]
+  int32_t N, Ne, Q;       // Ne = κ stride per term (N rounded up to a multiple of 4)
+  int32_t nchunks;        // TMA stages per row tile (8 κ each)
+  int32_t nsub;           // k4 sub-steps per row tile (= K / 4)
+  int32_t row_tiles;      // ceil(R / BN)
+  int32_t tiles_per_group;
+  int32_t ldu_s;          // shared-memory row stride of the u tile (≡ 8 mod 16)
+  int32_t stages;
+  double* out;            // [n][ldo]
+  int64_t ldo;
+  ThetaDesc th;
+};
+
+constexpr int kBM = 64, kBN = 128, kWM = 2, kWN = 4;
+constexpr int kContractThreads = (kWM * kWN + 1) * 32;
+
+// u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups
+__host__ __device__ inline int contract_ldu(int ne) { return ne + ((4 - ne % 16) + 16) % 16; }
+
+__host__ inline size_t contract_smem_bytes(int stages, int ldu, int q) {
+  return size_t(stages) * 2 * kBN * 4 * sizeof(double) + size_t(kBM) * ldu * sizeof(double) +
+         2 * size_t(q) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
+}
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    contract_kernel(const __grid_constant__ CUtensorMap tmap, const ContractParams p) {
+  constexpr int NCW = WM * WN;
+  constexpr int TM = BM / WM, TN = BN / WN;
+  constexpr int MI = TM / 8, NI = TN / 8;
+  constexpr int STAGE = 2 * BN * 4;  // doubles per stage: two [BN][4] boxes
+  static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile must be a multiple of 8x8");
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double* Sst = reinterpret_cast<double*>(smem_raw);
+  double* Us = Sst + size_t(p.stages) * STAGE;
+  double* thS = Us + size_t(BM) * p.ldu_s;
+  double* thnuS = thS + p.Q * BM;
+  uint64_t* full = reinterpret_cast<uint64_t*>(thnuS + p.Q * BM);
+  uint64_t* empty = full + p.stages;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile0 = blockIdx.x * BM;
+  const int rt_begin = blockIdx.y * p.tiles_per_group;
+  const int rt_end = min(p.row_tiles, rt_begin + p.tiles_per_group);
+  if (rt_begin >= rt_end) return;  // whole CTA, before any barrier
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == NCW && lane == 0) prefetch_tmap(&tmap);
+
+  // resident u tile (zero-padded in k and beyond the chunk) and θ, νθ for the tile's samples
+  for (int idx = threadIdx.x; idx < BM * p.ldu_s; idx += blockDim.x) {
+    const int b = idx / p.ldu_s, k = idx - b * p.ldu_s;
+    const int i = tile0 + b;
+    double v = 0.0;
+    if (i < p.n && k < p.N) v = p.u[int64_t(p.act ? p.act[i] : i) * p.N + k];
+    Us[idx] = v;
+  }
+  for (int b = threadIdx.x; b < BM; b += blockDim.x) {
+    const int i = tile0 + b;
+    if (i < p.n) {
+      const int id = p.act ? p.act[i] : i;
+      const double alpha = p.mu[2 * id], re = p.mu[2 * id + 1];
+      const double nu = 1.0 / re;
+      for (int q = 0; q < p.Q; ++q) {
+        const double th = eval_theta_term(p.th, q, alpha, re);
+        thS[q * BM + b] = th;
+        thnuS[q * BM + b] = nu * th;
+      }
+    } else {
+      for (int q = 0; q < p.Q; ++q) thS[q * BM + b] = thnuS[q * BM + b] = 0.0;
+    }
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ---------------- TMA producer (one elected lane) ----------------
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int rt = rt_begin; rt < rt_end; ++rt) {
+        for (int c = 0; c < p.nchunks; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], STAGE * sizeof(double));
+          double* dst = Sst + size_t(stage) * STAGE;
+          tma_load_2d(dst, &tmap, &full[stage], c * 8, rt * BN, pol);
+          tma_load_2d(dst + BN * 4, &tmap, &full[stage], c * 8 + 4, rt * BN, pol);
+          if (++stage == p.stages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers ----------------
+  const int wm = warp / WN, wn = warp % WN;
+  const int g = lane >> 2, t = lane & 3;
+  const int sb0 = wm * TM, rb0 = wn * TN;
+  const int kterms = p.Q * p.Ne;  // κ where the ν θ_q (linear) block starts
+  int stage = 0;
+  uint32_t phase = 0;
+
+  for (int rt = rt_begin; rt < rt_end; ++rt) {
+    double acc[MI][NI][2], accq[MI][NI][2];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
+
+    int q = 0, k0 = 0;  // current term and k offset of the sub-step (uniform over the warp)
+    for (int c = 0; c < p.nchunks; ++c) {
+      mbar_wait(&full[stage], phase);
+      const double* st = Sst + size_t(stage) * STAGE;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int kap = 8 * c + 4 * j;
+        if (kap >= 4 * p.nsub) break;
+        double af[MI], bf[NI];
+        if (kap < kterms) {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = Us[(sb0 + mi * 8 + g) * p.ldu_s + k0 + t];
+        } else {
+          const int lin = kap - kterms + t;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Q ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
+        }
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) bf[ni] = st[(j * BN + rb0 + ni * 8 + g) * 4 + t];
+        if (kap < kterms) {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(accq[mi][ni][0], accq[mi][ni][1], af[mi], bf[ni]);
+          k0 += 4;
+          if (k0 == p.Ne) {  // end of term q: acc += θ_q ∘ accq
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+              const double th = thS[q * BM + sb0 + mi * 8 + g];
+#pragma unroll
+              for (int ni = 0; ni < NI; ++ni) {
+                acc[mi][ni][0] = fma(th, accq[mi][ni][0], acc[mi][ni][0]);
+                acc[mi][ni][1] = fma(th, accq[mi][ni][1], acc[mi][ni][1]);
+                accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
+              }
+            }
+            k0 = 0;
+            ++q;
+          }
+        } else {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+        }
+      }
+      // release the stage once its fragments were consumed by the issued MMAs (register dependency)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == p.stages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    // epilogue: fragment (sample g, rows 2t..2t+1) -> out[sample][row] as 16-byte stores
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int i = tile0 + sb0 + mi * 8 + g;
+      if (i < p.n) {
+        double* o = p.out + int64_t(i) * p.ldo + int64_t(rt) * BN + rb0 + 2 * t;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+          *reinterpret_cast<double2*>(o + ni * 8) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      }
+    }
+  }
+}
+
+}  // namespace rbns
