@@ -1,0 +1,332 @@
+"""Benchmark: batched reduced Navier–Stokes online solves (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A *step* is one batched velocity-only Newton solve of the rank's μ shard for the chosen
+BASELINE.json config (default config 2: N=100, Q=7, 65536 μ per GPU), inputs resident in HBM.  Multi-GPU
+(torchrun, one process per GPU) shards μ with no collective on the solve path (weak scaling: every rank
+solves its own 65536-sample slice of one seeded μ stream); the only collectives are the timing barrier and
+the max-over-ranks reduction of the device time.
+
+The JSON line carries: value (whole-job solves/s, device-timed), e2e (same metric through the C-ABI host-buffer
+call rbns_solve_host with pinned host μ and results, copies inside the timed region), roofline (the DMMA
+contraction kernel against the FP64 peak measured live with cuBLAS DGEMM), cpu_baseline (the numpy oracle
+on the host cores, bounded sample), clocks (nvidia-smi sampled during the timed region) and gpu_launches.
+
+``--impl reference`` times the reference-side CPU implementation of the path (the oracle port in oracle/,
+batched numpy/BLAS form, all host threads; the reference ships no code for this path — SURVEY.md §0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "reduced Newton solves/sec (mu samples/s) at N=100,Q=7"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
+    ap.add_argument("--cpu-sample", type=int, default=1024, help="μ samples in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return world, rank, local
+
+
+def config_block(cfg, batch, world):
+    return {"workload": f"cfg{cfg.index}: N={cfg.n}, Q={cfg.q}, B={batch} per GPU"
+                        + (f", Np={cfg.n_p}" if cfg.n_p else ""),
+            "N": cfg.n, "Q": cfg.q, "Np": cfg.n_p, "batch_per_gpu": batch, "global_batch": batch * world,
+            "theta_family": cfg.theta_family, "tol": cfg.tol, "max_iter": cfg.max_iter,
+            "parallelism": f"mu-sharded x{world} (no collective on the solve path)",
+            "l2": "flushed between timed steps (256 MiB write); J (5.3 GB/iteration) streams through L2"}
+
+
+def cpu_baseline(cfg, model, mu, sample):
+    """Oracle batched path (numpy + multithreaded BLAS) on a bounded μ sample; returns solves/s."""
+    from oracle import rbns_oracle as oracle
+
+    S = oracle.symmetrised_operator(model)
+    oracle.solve_batch(model, mu[:min(32, sample)], tol=cfg.tol, max_iter=cfg.max_iter, S=S)  # warm-up
+    t0 = time.perf_counter()
+    oracle.solve_batch(model, mu[:sample], tol=cfg.tol, max_iter=cfg.max_iter, S=S)
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
+    except Exception:  # pragma: no cover
+        blas = []
+    return {"value": sample / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"{sample} mu of cfg{cfg.index} (first {sample} of the seeded stream), batched numpy/BLAS "
+                      f"oracle (oracle/rbns_oracle.py:solve_batch), {dt:.2f} s; BLAS: {', '.join(blas)}"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def fp64_peak(torch, device) -> dict:
+    """cuBLAS DGEMM 8192^3 best of 5 (burst), the FP64 roofline denominator measured in this run."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=device)
+    b = torch.randn(n, n, dtype=torch.float64, device=device)
+    torch.matmul(a, b)
+    torch.cuda.synchronize(device)
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize(device)
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return {"tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "source": "live cuBLAS DGEMM 8192^3 burst (this run)"}
+
+
+def traffic_from_profile(cfg_index: int):
+    p = ROOT / "profiles" / "contract_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(f"cfg{cfg_index}", {}).get("dram_bytes_per_launch")
+    except (ValueError, OSError):
+        return None
+
+
+def run_reference(args, cfg, world, rank):
+    from paper_1807_11866_b200 import synthetic
+    from oracle import rbns_oracle as oracle
+
+    if rank != 0:
+        return
+    model = synthetic.config_model(cfg)
+    batch = args.batch or cfg.batch
+    mu = synthetic.config_mu(cfg) if batch <= cfg.batch else synthetic.make_mu(batch, cfg.re_max)
+    sample = min(args.cpu_sample, batch)
+    S = oracle.symmetrised_operator(model)
+    for _ in range(args.warmup):
+        oracle.solve_batch(model, mu[:min(64, sample)], tol=cfg.tol, max_iter=cfg.max_iter, S=S)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.solve_batch(model, mu[:sample], tol=cfg.tol, max_iter=cfg.max_iter, S=S)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    value = sample / dt
+    cores = len(os.sched_getaffinity(0))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(cfg, batch, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{sample} mu per step of cfg{cfg.index}; batched numpy/BLAS oracle port "
+                                       "(reference ships no online code)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    from paper_1807_11866_b200 import online, synthetic
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+
+    batch = args.batch or cfg.batch
+    model = synthetic.config_model(cfg)
+    mu_all = synthetic.make_mu(batch * world, cfg.re_max)
+    mu_np = np.ascontiguousarray(mu_all[rank * batch:(rank + 1) * batch])
+    mu = torch.from_numpy(mu_np).to(device)
+    pressure = cfg.n_p > 0
+
+    dm = online.DeviceModel(model, local)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=device)
+    res = None
+    for _ in range(args.warmup):
+        res = dm.solve(mu, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=res)
+    torch.cuda.synchronize(device)
+
+    stream = torch.cuda.current_stream(device)
+    step_ms, gemm_ms, launches, contraction_its, gemm_launches = [], [], 0, 0, 0
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = dm.solve(mu, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=res)
+            e1.record(stream)
+            torch.cuda.synchronize(device)
+            step_ms.append(e0.elapsed_time(e1))
+            st = res.stats
+            gemm_ms.append(st["ms_gemm"])
+            launches += st["kernel_launches"]
+            contraction_its += st["contraction_iterations"]
+            gemm_launches += st["gemm_launches"]
+    torch.cuda.synchronize(device)
+    if dist is not None:
+        dist.barrier()
+    mean_ms = float(np.mean(step_ms))
+    t = torch.tensor([mean_ms], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+
+    # ---- end-to-end through the C-ABI with host buffers (pinned μ in, results out) ----
+    mu_pin = torch.from_numpy(mu_np).pin_memory()
+    n, npr = cfg.n, cfg.n_p
+    host = dict(u=torch.empty((batch, n), dtype=torch.float64).pin_memory(),
+                p=torch.empty((batch, npr), dtype=torch.float64).pin_memory() if pressure else None,
+                iters=torch.empty(batch, dtype=torch.int32).pin_memory(),
+                status=torch.empty(batch, dtype=torch.int8).pin_memory(),
+                last_update=torch.empty(batch, dtype=torch.float64).pin_memory())
+    host_np = {k: (v.numpy() if v is not None else None) for k, v in host.items()}
+    mu_pin_np = mu_pin.numpy()
+    dm.solve_host(mu_pin_np, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=host_np)
+    if dist is not None:
+        dist.barrier()
+    e2e_ms = []
+    for _ in range(max(1, args.steps)):
+        flush.zero_()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        dm.solve_host(mu_pin_np, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=host_np)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    h2d = batch * 2 * 8
+    d2h = batch * (n * 8 + 4 + 1 + 8) + (batch * npr * 8 if pressure else 0)
+
+    if rank == 0:
+        peak = fp64_peak(torch, device)
+        flops_per_launch = contraction_its / max(gemm_launches, 1) * 2.0 * cfg.q * cfg.n ** 3
+        achieved = contraction_its * 2.0 * cfg.q * cfg.n ** 3 / (sum(gemm_ms) * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "contract_kernel (DMMA.8x8x4 + TMA)", "achieved": achieved,
+                "peak": peak["tflops"], "unit": "TFLOP/s", "frac": achieved / peak["tflops"],
+                "peak_source": peak["source"], "traffic": traffic_from_profile(cfg.index),
+                "algorithmic_flops_per_launch": flops_per_launch,
+                "flops_rule": "2*Q*N^3 per sample-iteration with u != 0 (SURVEY.md §8(d)); first Newton step "
+                              "has u = 0 and runs no contraction",
+                "gemm_share_of_step": float(np.sum(gemm_ms) / np.sum(step_ms))}
+        line = {"metric": METRIC, "value": batch * world / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_block(cfg, batch, world),
+                "e2e": {"value": batch * world / (float(te.item()) * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                        "path": "rbns_solve_host (C-ABI), pinned host buffers"},
+                "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary(),
+                "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
+                           "converged": int((res.status == 0).sum().item()), "batch": batch}}
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, model, mu_np, min(args.cpu_sample, batch))
+        print(json.dumps(line), flush=True)
+    dm.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    from paper_1807_11866_b200 import synthetic
+
+    cfg = synthetic.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+    else:
+        run_ours(args, cfg, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -453,7 +453,9 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
   };
   if (m->smem > size_t(max_smem))
     return cleanup(fail(RBNS_ERR_UNSUPPORTED, "u tile does not fit shared memory for N=" + std::to_string(m->N)));
-  if (cudaFuncSetAttribute(kContract, cudaFuncAttributeMaxDynamicSharedMemorySize, int(m->smem)) != cudaSuccess)
+  // a per-function cap shared by every model: set it to the device maximum (not this model's size), so a
+  // model created later with a smaller tile cannot invalidate launches of an earlier one
+  if (cudaFuncSetAttribute(kContract, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) != cudaSuccess)
     return cleanup(fail(RBNS_ERR_CUDA, "cudaFuncSetAttribute(contract) failed"));
 
   // keep freed stream-ordered allocations pooled (no re-allocation between calls)

@@ -1,0 +1,74 @@
+"""CPU tests of the C-ABI boundary: the library builds, loads, exports every symbol include/rbns.h declares,
+and rejects bad arguments without touching a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1807_11866_b200 import build, _native
+
+    build.build()
+    return _native.load()
+
+
+def header_functions():
+    txt = (ROOT / "include" / "rbns.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(rbns_\w+)\s*\(", txt, re.M)))
+
+
+def test_header_lists_functions():
+    fns = header_functions()
+    assert "rbns_solve" in fns and "rbns_model_create" in fns and len(fns) >= 10
+
+
+def test_all_header_symbols_exported(lib):
+    from paper_1807_11866_b200 import _native
+
+    for name in header_functions():
+        assert hasattr(lib, name), f"{name} not exported"
+    assert set(header_functions()) == set(_native.EXPORTED_SYMBOLS)
+
+
+def test_abi_version_and_errors(lib):
+    assert lib.rbns_abi_version() == 1
+    assert lib.rbns_error_string(0) == b"ok"
+    assert b"invalid" in lib.rbns_error_string(1)
+    assert lib.rbns_error_string(99) == b"unknown error"
+
+
+def test_invalid_arguments_rejected_without_gpu(lib):
+    from paper_1807_11866_b200 import _native
+
+    out = ctypes.c_void_p()
+    assert lib.rbns_model_create(None, 0, ctypes.byref(out)) == 1
+    desc = _native.ModelDescC()
+    desc.n, desc.q = 0, 1
+    assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
+    assert b"N >= 1" in lib.rbns_last_error_message()
+    desc.n, desc.q = 10, 17
+    assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
+    assert lib.rbns_solve(None, None, 0, 1e-12, 20, None, None, None, None, None, None) == 1
+    assert lib.rbns_model_destroy(None) == 0
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    from paper_1807_11866_b200 import _native
+    from paper_1807_11866_b200.errors import NativeError
+
+    with pytest.raises(NativeError, match="not built"):
+        _native.load(tmp_path / "librbns.so")
+
+
+def test_struct_layouts_match_header():
+    from paper_1807_11866_b200 import _native
+
+    assert ctypes.sizeof(_native.ThetaTermC) == 24
+    assert ctypes.sizeof(_native.ModelDescC) == 16 + 6 * 8
+    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 32

@@ -1,0 +1,292 @@
+"""GPU parity tests: the sm_100a path through the C ABI against the CPU oracle and the golden fixtures.
+
+Bar (BASELINE.json north_star): relative error ≤ 1e-10 on velocity and pressure coefficients and identical
+Newton iteration counts.  Counts are compared exactly; a mismatch is tolerated only for a sample whose
+deciding update lies within 1e-6 relative of the stop threshold on the oracle side (knife-edge, reported).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import rbns_oracle as oracle  # noqa: E402
+from paper_1807_11866_b200 import affine, online, synthetic  # noqa: E402
+from paper_1807_11866_b200.errors import NativeError, SingularSystemError  # noqa: E402
+from paper_1807_11866_b200.model import ReducedModel  # noqa: E402
+
+from .golden_utils import golden, reference_model  # noqa: E402
+
+REL = 1e-10
+
+
+def rel_err(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def device_solve(dm, mu, **kw):
+    r = dm.solve(torch.from_numpy(np.ascontiguousarray(mu)).cuda(), **kw)
+    torch.cuda.synchronize()
+    return (r.u.cpu().numpy(), None if r.p is None else r.p.cpu().numpy(), r.iters.cpu().numpy(),
+            r.status.cpu().numpy(), r.last_update.cpu().numpy(), r.stats)
+
+
+def knife_edge(model, mu, tol=1e-12, max_iter=20, window=1e-6):
+    """Per-sample oracle margin: how close the deciding update was to the stop threshold."""
+    u = np.zeros(model.n)
+    for it in range(1, max_iter + 1):
+        R, J = oracle.reduced_operator(model, mu, u)
+        d = np.linalg.solve(J, -R)
+        u = u + d
+        ratio = np.linalg.norm(d) / (tol * np.linalg.norm(u))
+        if abs(ratio - 1.0) < window:
+            return True
+        if ratio <= 1.0:
+            return False
+    return False
+
+
+def check_counts(model, mu, it_dev, it_ref, tol=1e-12):
+    bad = np.nonzero(it_dev != it_ref)[0]
+    for b in bad:
+        assert knife_edge(model, mu[b], tol=tol), f"sample {b}: iters {it_dev[b]} vs oracle {it_ref[b]}"
+    return len(bad)
+
+
+@pytest.fixture(scope="module")
+def dms():
+    cache = {}
+
+    def get(key, model):
+        if key not in cache:
+            cache[key] = online.DeviceModel(model, 0)
+        return cache[key]
+
+    yield get
+    for dm in cache.values():
+        dm.close()
+
+
+# ---- golden fixtures -----------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("c", [0, 1, 2, 4])
+def test_golden_configs(cfg_model, dms, c):
+    d = golden(f"synthetic_cfg{c}")
+    cfg = synthetic.CONFIGS[c]
+    dm = dms(c, cfg_model(c))
+    u, p, it, st, last, stats = device_solve(dm, d["mu"], tol=cfg.tol, max_iter=cfg.max_iter)
+    assert np.all(st == 0)
+    assert rel_err(u, d["u"]) <= REL
+    assert np.array_equal(it, d["iters"])
+    if cfg.n_p:
+        assert rel_err(p, d["p"]) <= REL
+    assert stats["kernel_launches"] > 0 and stats["lu_launches"] > 0
+
+
+def test_reference_assembled_model(dms):
+    """Operator + solve on the reduced model built by the reference's own assembler (golden pin)."""
+    d = golden("reference_operator")
+    model = reference_model()
+    dm = dms("ref", model)
+    R, J = dm.reduced_operator(d["mu"], d["eta"])
+    R, J = R.cpu().numpy(), J.cpu().numpy()
+    for i in range(len(d["mu"])):
+        assert rel_err(R[i], d["R_ref"][i]) <= 1e-12
+        assert rel_err(J[i], d["J_ref"][i]) <= 1e-12
+    u, _, it, st, _, _ = device_solve(dm, d["solve_mu"])
+    assert np.all(st == 0) and np.array_equal(it, d["solve_iters"])
+    assert rel_err(u, d["solve_u"]) <= REL
+
+
+# ---- larger seeded slices against the oracle ---------------------------------------------------------
+
+@pytest.mark.parametrize("c,nb", [(0, 64), (1, 1024), (2, 384)])
+def test_parity_vs_oracle(cfg_model, dms, c, nb):
+    cfg = synthetic.CONFIGS[c]
+    model = cfg_model(c)
+    mu = synthetic.config_mu(cfg, nb)
+    u, _, it, st, last, _ = device_solve(dms(c, model), mu)
+    ur, itr, str_, _ = oracle.solve_batch(model, mu)
+    assert np.all(st == 0) and np.all(str_ == 0)
+    assert rel_err(u, ur) <= REL
+    check_counts(model, mu, it, itr)
+    assert np.all(last <= 1e-12 * np.linalg.norm(u, axis=1) * (1 + 1e-9))   # stop rule
+
+
+def test_pressure_recovery_parity(cfg_model, dms):
+    cfg = synthetic.CONFIGS[4]
+    model = cfg_model(4)
+    mu = synthetic.config_mu(cfg, 256)
+    u, p, it, st, _, _ = device_solve(dms(4, model), mu)
+    pr = oracle.recover_pressure(model, mu, u)
+    assert rel_err(p, pr) <= REL
+    # recovery alone, linearity
+    p1, _ = dms(4, model).recover_pressure(mu[:8], u[:8])
+    p2, _ = dms(4, model).recover_pressure(mu[:8], 2 * u[:8])
+    np.testing.assert_allclose(p2.cpu().numpy(), 2 * p1.cpu().numpy(), rtol=1e-13, atol=1e-13)
+
+
+def test_jacobian_finite_differences_device(cfg_model, dms):
+    model = cfg_model(1)
+    dm = dms(1, model)
+    rng = np.random.default_rng(11)
+    mu = np.array([[0.3, 120.0]])
+    eta = rng.standard_normal((1, model.n))
+    _, J = dm.reduced_operator(mu, eta)
+    J = J[0].cpu().numpy()
+    h = 1e-6
+    E = np.eye(model.n) * h
+    Rp, _ = dm.reduced_operator(np.repeat(mu, model.n, 0), eta + E)
+    Rm, _ = dm.reduced_operator(np.repeat(mu, model.n, 0), eta - E)
+    Jfd = ((Rp - Rm).cpu().numpy() / (2 * h)).T
+    assert np.abs(J - Jfd).max() <= 1e-6 * np.abs(J).max()
+    R0, J0 = dm.reduced_operator(mu, np.zeros((1, model.n)))      # η = 0 KAT
+    th = affine.evaluate_weights(model.theta, mu)[0]
+    np.testing.assert_allclose(R0[0].cpu().numpy(), -(th @ model.f), atol=1e-13)
+
+
+# ---- full BASELINE sizes: size-independent properties ------------------------------------------------
+
+def test_full_batch_cfg2_properties(cfg_model, dms):
+    cfg = synthetic.CONFIGS[2]
+    model = cfg_model(2)
+    dm = dms(2, model)
+    mu = synthetic.config_mu(cfg)
+    mud = torch.from_numpy(mu).cuda()
+    r1 = dm.solve(mud)
+    u1, it1, st1 = r1.u.clone(), r1.iters.clone(), r1.status.clone()
+    r2 = dm.solve(mud)
+    assert torch.equal(u1, r2.u) and torch.equal(it1, r2.iters)          # bitwise determinism
+    assert int((st1 == 0).sum()) == cfg.batch                            # all 65536 converge
+    # batch-composition invariance: a strided subset solved alone is bitwise identical
+    idx = torch.arange(7, cfg.batch, 97, device="cuda")
+    r3 = dm.solve(mud[idx])
+    assert torch.equal(r3.u, u1[idx]) and torch.equal(r3.iters, it1[idx])
+    # residual at the solution (size-independent): ‖R(u)‖ ≤ 1e-9 ‖f‖ on a subset
+    sub = idx[:512]
+    R, _ = dm.reduced_operator(mud[sub], u1[sub])
+    th = affine.evaluate_weights(model.theta, mu[sub.cpu().numpy()])
+    fn = np.linalg.norm(th @ model.f, axis=1)
+    assert np.all(np.linalg.norm(R.cpu().numpy(), axis=1) <= 1e-9 * fn)
+    # oracle parity on a random subset of the full batch
+    rng = np.random.default_rng(0)
+    pick = np.sort(rng.choice(cfg.batch, 256, replace=False))
+    ur, itr, _, _ = oracle.solve_batch(model, mu[pick])
+    assert rel_err(u1.cpu().numpy()[pick], ur) <= REL
+    check_counts(model, mu[pick], it1.cpu().numpy()[pick], itr)
+
+
+# ---- edge cases the SPEC names -------------------------------------------------------------------------
+
+def _tiny(n=6, q=2, c_scale=0.0, a_scale=1.0, f_scale=1.0, seed=0, **kw):
+    rng = np.random.default_rng(seed)
+    A = a_scale * np.stack([np.eye(n) * (1 + i) for i in range(q)])
+    C = c_scale * rng.standard_normal((q, n, n, n))
+    f = f_scale * rng.standard_normal((q, n))
+    return ReducedModel(A=A, C=C, f=f, theta=affine.family("trig3")[:q], **kw)
+
+
+def test_edge_batch_sizes_and_max_iter(cfg_model, dms):
+    dm = dms(0, cfg_model(0))
+    mu = synthetic.config_mu(0)
+    r = dm.solve(torch.zeros((0, 2), dtype=torch.float64, device="cuda"))
+    assert r.u.shape == (0, 10)
+    u, _, it, st, _, _ = device_solve(dm, mu[:1])
+    ur, itr, _, _ = oracle.solve_batch(cfg_model(0), mu[:1])
+    assert rel_err(u, ur) <= REL and it[0] == itr[0]
+    u, _, it, st, last, _ = device_solve(dm, mu, max_iter=0)
+    assert np.all(st == 1) and np.all(it == 0) and not u.any() and np.all(np.isnan(last))
+    u, _, it, st, _, _ = device_solve(dm, mu, max_iter=2)
+    assert np.all(st == 1) and np.all(it == 2)
+
+
+def test_edge_outcomes():
+    mu = np.array([[0.1, 20.0], [0.2, 50.0]])
+    with online.DeviceModel(_tiny(a_scale=0.0), 0) as dm:            # J = 0: singular
+        _, _, it, st, _, _ = device_solve(dm, mu)
+        assert np.all(st == 2) and np.all(it == 1)
+    with online.DeviceModel(_tiny(f_scale=0.0), 0) as dm:            # f = 0: u = 0 in one step
+        u, _, it, st, _, _ = device_solve(dm, mu)
+        assert np.all(st == 0) and np.all(it == 1) and not u.any()
+    with online.DeviceModel(_tiny(), 0) as dm:                       # Re = 0 → ν = inf
+        _, _, _, st, _, _ = device_solve(dm, np.array([[0.1, 0.0]]))
+        assert st[0] in (2, 4)
+    bad_mp = _tiny(Mp=-np.eye(3), Bq=np.ones((2, 3, 6)))             # B_sp not SPD → SINGULAR_RECOVERY
+    with online.DeviceModel(bad_mp, 0) as dm:
+        _, p, _, st, _, _ = device_solve(dm, mu)
+        assert np.all(st == 3) and np.all(np.isnan(p))
+    with online.DeviceModel(_tiny(), 0) as dm:                       # p requested, model has no Np
+        mu_d = torch.from_numpy(mu).cuda()
+        out = [torch.empty(2, 6, dtype=torch.float64, device="cuda"), torch.empty(2, 6, dtype=torch.float64, device="cuda"),
+               torch.empty(2, dtype=torch.int32, device="cuda"), torch.empty(2, dtype=torch.int8, device="cuda"),
+               torch.empty(2, dtype=torch.float64, device="cuda")]
+        rc = dm.lib.rbns_solve(dm._h, mu_d.data_ptr(), 2, 1e-12, 20, *[t.data_ptr() for t in out], None)
+        assert rc == 5
+        with pytest.raises(NativeError):
+            from paper_1807_11866_b200 import _native
+            _native.check(rc, "rbns_solve")
+
+
+def _random_model(n, q, seed):
+    """Generator-style model (SURVEY.md Appendix B scalings) with q terms drawn from the Fourier + monomial
+    families, for shapes outside the BASELINE configs."""
+    rng = np.random.default_rng(seed)
+    terms = (affine.family("fourier13") + affine.monomials([(1, 0), (0, 1), (2, 0)], [1.0, 1e-3, 0.5]))[:q]
+    G = rng.standard_normal((n, n))
+    A = [G @ G.T / n + np.eye(n)]
+    for _ in range(1, q):
+        S = rng.standard_normal((n, n))
+        A.append(0.1 * (S + S.T) / 2 / np.sqrt(n))
+    C = 1e-5 / n * rng.standard_normal((q, n, n, n))
+    C = 0.5 * (C - C.transpose(0, 1, 3, 2))
+    return ReducedModel(A=np.stack(A), C=C, f=rng.standard_normal((q, n)), theta=terms)
+
+
+@pytest.mark.parametrize("n,q", [(7, 1), (13, 3), (33, 5), (64, 16), (127, 2)])
+def test_odd_and_extreme_shapes(n, q):
+    model = _random_model(n, q, seed=n)
+    mu = synthetic.make_mu(40, 100.0, seed=n)
+    with online.DeviceModel(model, 0) as dm:
+        u, _, it, st, _, _ = device_solve(dm, mu)
+    ur, itr, str_, _ = oracle.solve_batch(model, mu)
+    assert np.array_equal(st, str_)
+    assert rel_err(u, ur) <= REL
+    check_counts(model, mu, it, itr)
+
+
+def test_monomial_family_and_single_query(dms):
+    model = reference_model()
+    sol = online.solve_block(model, (0.2, 4.0))
+    u, it, st, _ = oracle.solve_sample(model, np.array([0.2, 4.0]))
+    assert sol.converged and sol.newton_iters == it and not sol.s_coeffs.any()
+    assert rel_err(sol.u_coeffs, u) <= REL
+    assert set(sol.wall_time) >= {"assembly", "solve", "recovery"}
+    with pytest.raises(SingularSystemError):
+        online.solve_block(_tiny(a_scale=0.0), (0.1, 10.0))
+
+
+def test_zero_quadrature_online(cfg_model, dms):
+    """The online path performs no quadrature (instrument.py:3-5)."""
+    from paper_1807_11866_b200 import instrument
+
+    before = instrument.quadrature_evals()
+    device_solve(dms(0, cfg_model(0)), synthetic.config_mu(0))
+    assert instrument.quadrature_evals() == before
+
+
+def test_concurrent_streams(cfg_model, dms):
+    """Two solves on two streams with one shared read-only model."""
+    dm = dms(1, cfg_model(1))
+    mu = torch.from_numpy(synthetic.config_mu(1, 512)).cuda()
+    ref = dm.solve(mu)
+    ref_u = ref.u.clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        a = dm.solve(mu[:256], stream=s1)
+    with torch.cuda.stream(s2):
+        b = dm.solve(mu[256:], stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([a.u, b.u]), ref_u)
