@@ -12,7 +12,7 @@ from pathlib import Path
 
 from .errors import NativeError
 
-LIB_PATH = Path(__file__).resolve().parent / "librbns.so"
+LIB_PATH = Path(os.environ.get("RBNS_LIB", Path(__file__).resolve().parent / "librbns.so"))
 
 MAX_TERMS = 16
 STATUS_NAMES = {0: "CONVERGED", 1: "NON_CONVERGED", 2: "SINGULAR_SYSTEM", 3: "SINGULAR_RECOVERY", 4: "NONFINITE"}

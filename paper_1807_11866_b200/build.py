@@ -29,17 +29,21 @@ def _nvcc() -> str:
     return str(cand) if cand.exists() else "nvcc"
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=()) -> Path:
+    """Compile csrc/*.cu into ``out`` (default: the in-tree librbns.so); ``extra`` adds nvcc flags
+    (e.g. -DRBNS_TRACE for the instrumented development build)."""
+    OUT_ = Path(out)
     srcs = sorted(CSRC.glob("*.cu"))
     deps = srcs + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "rbns.h"]
-    if OUT.exists() and not force and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in deps):
-        return OUT
-    OBJ.mkdir(parents=True, exist_ok=True)
+    if OUT_.exists() and not force and all(OUT_.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return OUT_
+    obj_dir = OBJ if not extra else OBJ.parent / ("obj_" + "_".join(x.strip("-D").lower() for x in extra))
+    obj_dir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,14 +55,17 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = OUT_.with_suffix(".so.tmp")
     r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
                         *map(str, objs)], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, OUT_)
+    return OUT_
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--trace" in sys.argv:
+        print(build(force="-f" in sys.argv, out=ROOT / "build" / "librbns_trace.so", extra=("-DRBNS_TRACE",)))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -94,6 +94,18 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
 }
 
+// Reciprocal for pivots: hardware approximation (MUFU.RCP64H) refined by two Newton–Raphson steps
+// (~23 → ~46 → full 53 bits, within 1 ulp of 1/x).  Callers guarantee x is finite, nonzero and normal;
+// it replaces the IEEE division sequence on the serial critical path of the Gauss–Jordan column steps.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // FP64 tensor-core MMA (lowers to DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) * B(4x8).
 // Thread (g = lane>>2, t = lane&3) supplies A[g][t], B[t][g]; holds D[g][2t], D[g][2t+1].
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {

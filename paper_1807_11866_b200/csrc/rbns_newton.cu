@@ -2,6 +2,10 @@
 // (rbns_newton.cuh); kept in its own translation unit so the instantiations compile in parallel with the rest
 // of the library.  A few fixed shapes cover every N ≤ 127 (RS·TGR ≥ N rows, CS·TGC ≥ N+1 columns).
 #include "rbns_launch.h"
+#include <cstdlib>
+#include <cstring>
+
+#include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
 
 namespace rbns {
@@ -28,11 +32,56 @@ const Shape* plan(int N) {
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
   return nullptr;
 }
+
+// blocked (DMMA) variant: RT×CT tiles of 8×8, NW warps
+struct BShape {
+  int rt, ct, nw;
+  NewtonKernel kern;
+  size_t smem;
+};
+
+#define RBNS_BS(R_, C_, W_) {R_, C_, W_, newton_bgj_kernel<R_, C_, W_>, sizeof(BGJShared<R_, C_, W_>)}
+const BShape kBShapes[] = {
+    RBNS_BS(2, 2, 2),     // N ≤ 15
+    RBNS_BS(7, 7, 4),     // N ≤ 55
+    RBNS_BS(13, 13, 8),   // N ≤ 103
+    RBNS_BS(16, 16, 8),   // N ≤ 127
+};
+#undef RBNS_BS
+
+const BShape* bplan(int N) {
+  for (const BShape& s : kBShapes)
+    if (N >= 1 && N <= 8 * s.rt && N + 1 <= 8 * s.ct) return &s;
+  return nullptr;
+}
+
+// RBNS_NEWTON=bgj selects the blocked DMMA kernel (rbns_bgj.cuh); the default is the rank-1 register kernel
+// (rbns_newton.cuh), currently the faster of the two at N ≤ 104 (both are parity-tested).
+bool use_blocked() {
+  static const bool blocked = [] {
+    const char* v = std::getenv("RBNS_NEWTON");
+    return v && std::strcmp(v, "bgj") == 0;
+  }();
+  return blocked;
+}
 }  // namespace
 
-bool newton_supported(int N) { return plan(N) != nullptr; }
+bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr; }
 
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
+  if (use_blocked()) {
+    if (const BShape* b = bplan(p.N)) {
+      static bool attr_set[sizeof(kBShapes) / sizeof(kBShapes[0])] = {};
+      const int idx = int(b - kBShapes);
+      if (!attr_set[idx]) {  // benign race: idempotent attribute
+        cudaError_t e = cudaFuncSetAttribute(b->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(b->smem));
+        if (e != cudaSuccess) return e;
+        attr_set[idx] = true;
+      }
+      b->kern<<<p.n, b->nw * 32, b->smem, st>>>(p);
+      return cudaGetLastError();
+    }
+  }
   const Shape* s = plan(p.N);
   if (!s) return cudaErrorInvalidValue;
   s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
@@ -40,3 +89,9 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
 }
 
 }  // namespace rbns
+
+#ifdef RBNS_TRACE
+extern "C" int rbns_debug_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, rbns::g_trace, sizeof(unsigned long long) * (n < 256 ? n : 256)) == cudaSuccess ? 0 : 2;
+}
+#endif
