@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU session: bench line, plain run + ncu launch list of one bench step, full ncu capture of the two hot kernels.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
+python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
+$CMD > gpurun_out/plain.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+P="python tools/profile_case.py 2 65536"
+$P > gpurun_out/plain2.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"contract_kernel|newton_gj" -s 4 -c 2 -o gpurun_out/full $P > gpurun_out/ncu_full.log 2>&1
+tail -2 gpurun_out/ncu_full.log
