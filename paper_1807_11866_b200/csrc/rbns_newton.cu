@@ -7,6 +7,7 @@
 
 #include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
+#include "rbns_newton_cluster.cuh"
 
 namespace rbns {
 
@@ -66,7 +67,10 @@ bool use_blocked() {
 }
 }  // namespace
 
-bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr; }
+// N > 127: the 2-CTA cluster kernel (rbns_newton_cluster.cuh), 16×(2×16) threads, N ≤ 207
+constexpr int kClusterMaxN = 207;
+
+bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
 
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
   if (use_blocked()) {
@@ -83,6 +87,10 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
     }
   }
   const Shape* s = plan(p.N);
+  if (!s && p.N <= kClusterMaxN) {
+    newton_gjc_kernel<16, 16, 13, 7><<<2 * p.n, 256, 0, st>>>(p);
+    return cudaGetLastError();
+  }
   if (!s) return cudaErrorInvalidValue;
   s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
   return cudaGetLastError();

@@ -1,0 +1,281 @@
+// rbns_newton_cluster.cuh — K3 for large N (config 3, N = 200): the register Gauss–Jordan Newton update of
+// rbns_newton.cuh spread over a 2-CTA thread-block cluster (two SMs), because [J | −R] (200×201 fp64,
+// 322 KB) does not fit one SM's register file.
+//
+// Each CTA holds ALL rows and half of the columns: global thread-column tc_g = 16·rank + tc (32 in total),
+// column j lives in CTA (j mod 32)/16, thread-column j mod 16, slot j/32; rows tr + 16·r as before.
+// Per column step the owner half-warp (one CTA) publishes the pivot column and the pivot choice into BOTH
+// CTAs' shared memory (DSMEM stores through the cluster window), one cluster barrier makes them visible,
+// each CTA's pivot-row owners publish their half of the pivot row locally, one CTA barrier, register DFMA
+// update.  The cluster barrier is the price of the second SM; partial pivoting is unchanged.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "rbns_common.cuh"
+#include "rbns_newton.cuh"
+
+namespace rbns {
+
+template <int TGR, int TGC, int RS, int CS>
+struct GJCShared {
+  static constexpr int NW = TGR * TGC / 32;
+  static constexpr int CBS = RS | 1;
+  double th[RBNS_MAX_TERMS];
+  double nu;
+  double pv[2];
+  int pk[2];
+  double colbuf[2][TGR][CBS];
+  double P[CS][TGC];
+  double piv[TGR * RS];
+  int perm[TGR * RS];
+  double rhs[TGR * RS];
+  double rowred[NW][TGR * RS];
+  double xred[2][TGR * RS];  // per-rank partial J·u row sums, collected in the RHS-owner CTA
+  double red[2][NW];
+};
+
+template <int TGR, int TGC, int RS, int CS, int SB>
+__device__ __forceinline__ void gjc_block(double (&a)[RS][CS], unsigned& pmask, bool& sing, const int N,
+                                          const int tr, const int tc, const int rank, GJCShared<TGR, TGC, RS, CS>& sh,
+                                          GJCShared<TGR, TGC, RS, CS>* peer) {
+  namespace cg = cooperative_groups;
+  if constexpr (SB < CS) {
+    if (sing) return;
+#pragma unroll 1
+    for (int kk = 0; kk < 2 * TGC; ++kk) {
+      const int k = SB * 2 * TGC + kk;
+      if (k >= N) return;
+      const int buf = k & 1;
+      const int oc = kk / TGC, otc = kk % TGC;
+      if (rank == oc && tc == otc) {
+        // owner half-warp: publish column k to both CTAs, argmax of |a| over unpivoted rows
+        long long best = -1;
+        double bsig = 0.0;
+        int bi = -1;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+          const double v = a[r][SB];
+          sh.colbuf[buf][tr][r] = v;
+          peer->colbuf[buf][tr][r] = v;
+          const long long key =
+              (((pmask >> r) & 1u) || tr + TGR * r >= N) ? -1LL : __double_as_longlong(fabs(v));
+          if (key > best) {
+            best = key;
+            bsig = v;
+            bi = tr + TGR * r;
+          }
+        }
+        const unsigned gmask = ((1u << TGR) - 1u) << ((otc * TGR) & 31);
+#pragma unroll
+        for (int o = TGR / 2; o > 0; o >>= 1) {
+          const long long k2 = __shfl_xor_sync(gmask, best, o);
+          const double s2 = __shfl_xor_sync(gmask, bsig, o);
+          const int i2 = __shfl_xor_sync(gmask, bi, o);
+          if (k2 > best || (k2 == best && k2 >= 0 && i2 < bi)) {
+            best = k2;
+            bsig = s2;
+            bi = i2;
+          }
+        }
+        const bool ok = best > 0 && best < 0x7ff0000000000000LL;  // nonzero, finite
+        __syncwarp(gmask);
+        if (ok && tr == bi % TGR) {  // the pivot row itself is not updated
+          sh.colbuf[buf][tr][bi / TGR] = 0.0;
+          peer->colbuf[buf][tr][bi / TGR] = 0.0;
+        }
+        if (tr == 0) {
+          sh.pk[buf] = ok ? bi : -1;
+          sh.pv[buf] = bsig;
+          peer->pk[buf] = ok ? bi : -1;
+          peer->pv[buf] = bsig;
+          sh.perm[k] = bi;
+          sh.piv[k] = bsig;
+          peer->perm[k] = bi;
+          peer->piv[k] = bsig;
+        }
+      }
+      cg::this_cluster().sync();
+      const int p = sh.pk[buf];
+      if (p < 0) {  // uniform across the cluster
+        sing = true;
+        return;
+      }
+      const double piv = sh.pv[buf];
+      const int tp = p % TGR, rp = p / TGR;
+      if (tr == tp) {
+        publish_row<RS, CS, SB, TGC>(a, rp, &sh.P[0][tc]);
+        pmask |= 1u << rp;
+      }
+      __syncthreads();
+      const double rpiv = 1.0 / piv;
+      double pj[CS];
+#pragma unroll
+      for (int s = SB; s < CS; ++s) pj[s] = sh.P[s][tc];
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        const double l = sh.colbuf[buf][tr][r] * rpiv;
+#pragma unroll
+        for (int s = SB; s < CS; ++s) a[r][s] = fma(-l, pj[s], a[r][s]);
+      }
+    }
+    gjc_block<TGR, TGC, RS, CS, SB + 1>(a, pmask, sing, N, tr, tc, rank, sh, peer);
+  }
+}
+
+template <int TGR, int TGC, int RS, int CS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
+    newton_gjc_kernel(const NewtonParams p) {
+  namespace cg = cooperative_groups;
+  constexpr int NT = TGR * TGC;
+  constexpr int NW = NT / 32;
+  static_assert(TGR == 16 && NT % 32 == 0, "owner half-warp layout needs TGR = 16");
+  __shared__ GJCShared<TGR, TGC, RS, CS> sh;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = int(cluster.block_rank());
+  GJCShared<TGR, TGC, RS, CS>* peer = cluster.map_shared_rank(&sh, rank ^ 1);
+  const int i_s = blockIdx.x / 2;
+  const bool live = i_s < p.n;  // both CTAs of a cluster agree
+  const int b = live ? p.act[i_s] : 0;
+  const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
+  const int N = p.N;
+  const int rhs_rank = (N % (2 * TGC)) / TGC, rhs_tc = N % TGC, rhs_slot = N / (2 * TGC);
+  auto gcol = [&](int s) { return s * 2 * TGC + rank * TGC + tc; };
+
+  if (tid == 0 && live) {
+    const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
+    sh.nu = 1.0 / re;
+    for (int q = 0; q < p.Q; ++q) sh.th[q] = eval_theta_term(p.th, q, alpha, re);
+  }
+  __syncthreads();
+  if (!live) {
+    cluster.sync();
+    return;
+  }
+  const double nu = sh.nu;
+
+  double a[RS][CS];
+  const double* Jb = p.J + int64_t(i_s) * p.ldj;
+#pragma unroll
+  for (int r = 0; r < RS; ++r)
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      const int i = tr + TGR * r, j = gcol(s);
+      double v = 0.0;
+      if (i < N && j < N) {
+        if (p.first) {
+          double acc = 0.0;
+#pragma unroll 1
+          for (int q = 0; q < p.Q; ++q) acc = fma(sh.th[q], __ldg(&p.A[(int64_t(q) * N + i) * N + j]), acc);
+          v = nu * acc;
+        } else {
+          v = __ldcs(&Jb[int64_t(i) * N + j]);
+        }
+      }
+      a[r][s] = v;
+    }
+
+  // right-hand side −R = f − ½ J u − ½ ν A(μ)u as column N (owned by CTA rhs_rank)
+  {
+    double uj[CS];
+#pragma unroll
+    for (int s = 0; s < CS; ++s) {
+      const int j = gcol(s);
+      uj[s] = (!p.first && j < N) ? p.u[int64_t(b) * N + j] : 0.0;
+    }
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      double part = 0.0;
+#pragma unroll
+      for (int s = 0; s < CS; ++s) part = fma(a[r][s], uj[s], part);
+#pragma unroll
+      for (int o = TGR; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane < TGR) sh.rowred[warp][tr + TGR * r] = part;
+    }
+    __syncthreads();
+    GJCShared<TGR, TGC, RS, CS>* own = rank == rhs_rank ? &sh : peer;
+    for (int i = tid; i < TGR * RS; i += NT) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += sh.rowred[w][i];
+      own->xred[rank][i] = s;
+    }
+    cluster.sync();
+    if (rank == rhs_rank) {
+      for (int i = tid; i < TGR * RS; i += NT) {
+        double rhs = 0.0;
+        if (i < N) {
+          const double ju = sh.xred[0][i] + sh.xred[1][i];
+          double fi = 0.0;
+#pragma unroll 1
+          for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
+          const double h = p.first ? 0.0 : Jb[int64_t(N) * N + i];
+          rhs = fi - 0.5 * ju - 0.5 * nu * h;
+        }
+        sh.rhs[i] = rhs;
+      }
+      __syncthreads();
+      if (tc == rhs_tc) {
+#pragma unroll
+        for (int r = 0; r < RS; ++r)
+#pragma unroll
+          for (int s = 0; s < CS; ++s)
+            if (s == rhs_slot) a[r][s] = sh.rhs[tr + TGR * r];
+      }
+    }
+  }
+
+  unsigned pmask = 0;
+  bool sing = false;
+  gjc_block<TGR, TGC, RS, CS, 0>(a, pmask, sing, N, tr, tc, rank, sh, peer);
+
+  if (rank == rhs_rank) {
+    if (!sing && tc == rhs_tc) {
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+#pragma unroll
+        for (int s = 0; s < CS; ++s)
+          if (s == rhs_slot) sh.rhs[tr + TGR * r] = a[r][s];
+    }
+    __syncthreads();
+    double d2 = 0.0, un2 = 0.0;
+    if (!sing) {
+      for (int k = tid; k < N; k += NT) {
+        const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
+        const double unew = (p.first ? 0.0 : p.u[int64_t(b) * N + k]) + x;
+        d2 = fma(x, x, d2);
+        un2 = fma(unew, unew, un2);
+      }
+    }
+    d2 = block_sum<NT>(d2, sh.red[0]);
+    un2 = block_sum<NT>(un2, sh.red[1]);
+    const bool finite = isfinite(d2) && isfinite(un2);
+    if (!sing && finite) {
+      for (int k = tid; k < N; k += NT) {
+        const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
+        const double uold = p.first ? 0.0 : p.u[int64_t(b) * N + k];
+        p.u[int64_t(b) * N + k] = uold + x;
+      }
+    }
+    if (tid == 0) {
+      int st;
+      if (sing)
+        st = RBNS_SINGULAR_SYSTEM;
+      else if (!finite)
+        st = RBNS_NONFINITE;
+      else if (sqrt(d2) <= p.tol * sqrt(un2))
+        st = RBNS_CONVERGED;
+      else if (p.iter >= p.max_iter)
+        st = RBNS_NON_CONVERGED;
+      else
+        st = kStatusActive;
+      p.status[b] = int8_t(st);
+      p.iters[b] = p.iter;
+      if (!sing && finite) p.last[b] = sqrt(d2);
+    }
+  }
+  cluster.sync();  // the peer may still read this CTA's shared memory
+}
+
+}  // namespace rbns

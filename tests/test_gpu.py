@@ -71,7 +71,7 @@ def dms():
 
 # ---- golden fixtures -----------------------------------------------------------------------------------
 
-@pytest.mark.parametrize("c", [0, 1, 2, 4])
+@pytest.mark.parametrize("c", [0, 1, 2, 3, 4])
 def test_golden_configs(cfg_model, dms, c):
     d = golden(f"synthetic_cfg{c}")
     cfg = synthetic.CONFIGS[c]

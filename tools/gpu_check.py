@@ -48,3 +48,6 @@ if __name__ == "__main__":
     timing(1)
     timing(2)
     timing(4)
+    if "cfg3" in sys.argv:
+        check(3, 64)
+        timing(3, reps=1)
