@@ -86,12 +86,13 @@ typedef struct rbns_stats {
   int64_t contraction_iterations; /* sample-iterations that ran the convective GEMM (iter >= 2)    */
   int32_t newton_rounds;          /* outer iterations executed (max over samples)                  */
   int32_t kernel_launches;        /* CUDA kernels launched by the call                             */
-  int32_t gemm_launches;          /* launches of the DMMA contraction kernel                       */
+  int32_t gemm_launches;          /* launches of the DMMA contraction kernel (incl. the u = 0 step) */
   int32_t lu_launches;            /* launches of the Newton-update (Gauss-Jordan) kernel           */
   double ms_gemm;                 /* device time (CUDA events) in the contraction kernel          */
   double ms_lu;                   /* device time in the Newton-update kernel                      */
   double ms_recovery;             /* device time in pressure recovery                             */
   double ms_total;                /* device time of the whole call (excluding host copies)        */
+  double ms_assembly;             /* device time of the u = 0 step's affine assembly (J = nu A(mu)) */
 } rbns_stats;
 
 /* Copy operators to `device`, build the symmetrised GEMM operand S_q = C_q + C_q^(12),

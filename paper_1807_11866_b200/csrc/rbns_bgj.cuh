@@ -30,17 +30,7 @@
 
 namespace rbns {
 
-#ifdef RBNS_TRACE
-__device__ unsigned long long g_trace[256];
-#define RBNS_TR(slot)                                                               \
-  do {                                                                              \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_trace[(slot) & 255] = clock64(); \
-  } while (0)
-#else
-#define RBNS_TR(slot) \
-  do {                \
-  } while (0)
-#endif
+
 
 template <int RT, int CT, int NW>
 struct BGJShared {
@@ -115,6 +105,8 @@ __device__ __forceinline__ void bgj_compute_w(int buf, int done, BGJShared<RT, C
 // c is lane c's pr[0][0].  Every lane computes the reciprocal of its own pr[0][0] right after the previous
 // update (no broadcast before the reciprocal), then the pivot lane's values are shuffled out.  The register
 // panel is rotated left after each column so the current column is always slot 0 (loop not unrolled).
+// Verification compares the high words of |a| (sign-cleared IEEE bits: exponent + 20 mantissa bits); only
+// an equal high word needs the exact 64-bit comparison.
 template <int RT, int CT, int NW>
 __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared<RT, CT, NW>& sh) {
   constexpr int NR = 8 * RT;
@@ -125,6 +117,7 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
   const int nc = min(8, N - 8 * P);
   if (nc < 8) {  // full panels overwrite every multiplier column
     for (int e = lane; e < NR * 8; e += 32) (&sh.L[buf][0][0])[e] = 0.0;
+    __syncwarp();
   }
   int rr[RPL];
   double pr[RPL][8];
@@ -134,7 +127,6 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) pr[s][cc] = rr[s] < NR ? sh.panel[rr[s] * PS + cc] : 0.0;
   }
-  __syncwarp();
   int c = 0;
   bool bad = false;
 #pragma unroll 1
@@ -147,16 +139,22 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
 #pragma unroll
     for (int cc = 1; cc < 8; ++cc) prow[cc] = __shfl_sync(0xffffffffu, pr[0][cc], c);
     // verification: no row below k (not yet pivoted) may beat |piv|
-    unsigned long long best = 0;
+    const int phi = __double2hiint(piv) & 0x7fffffff;
+    int bh = 0;
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
-      const unsigned long long key = (rr[s] > k && rr[s] < N)
-                                         ? (unsigned long long)__double_as_longlong(fabs(pr[s][0]))
-                                         : 0ull;
-      best = key > best ? key : best;
+      const int h = (rr[s] > k && rr[s] < N) ? (__double2hiint(pr[s][0]) & 0x7fffffff) : 0;
+      bh = max(bh, h);
     }
-    const unsigned long long pkey = (unsigned long long)__double_as_longlong(fabs(piv));
-    bad = __ballot_sync(0xffffffffu, best > pkey) != 0u;
+    unsigned gt = __ballot_sync(0xffffffffu, bh > phi);
+    if (__ballot_sync(0xffffffffu, bh == phi)) {  // rare: equal high words, compare exactly
+      bool g = false;
+#pragma unroll
+      for (int s = 0; s < RPL; ++s)
+        g |= rr[s] > k && rr[s] < N && fabs(pr[s][0]) > fabs(piv);
+      gt |= __ballot_sync(0xffffffffu, g);
+    }
+    bad = gt != 0u;
     if (bad || !(fabs(piv) >= 2.2250738585072014e-308) || !isfinite(piv)) break;  // warp-uniform
     double l[RPL];
 #pragma unroll
@@ -171,11 +169,11 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
       for (int cc = 1; cc < 7; ++cc) pr[s][cc] = fma(-l[s], prow[cc + 1], pr[s][cc + 1]);  // update + rotate
       pr[s][7] = 0.0;
     }
-    if (lane == 0) {
-      sh.perm[k] = k;
-      sh.pivval[k] = piv;
-      sh.prow[buf][c] = k;
-    }
+    if (lane == 0) sh.pivval[k] = piv;
+  }
+  if (lane < 8) {
+    sh.prow[buf][lane] = 8 * P + lane;
+    if (lane < c) sh.perm[8 * P + lane] = 8 * P + lane;
   }
   if (lane == 0) {
     sh.nc[buf] = c;
@@ -191,7 +189,28 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
     for (int s = 0; s < RPL; ++s)
       if (rr[s] < NR) sh.rhs[rr[s]] = pr[s][0];
   }
-  bgj_compute_w<RT, CT, NW>(buf, c, sh);
+  __syncwarp();
+  // W = T⁻¹, T[cc][c2] = l_{8P+cc, c2} = −L[8P+cc][c2] (pivot rows in natural order): all 28 entries are
+  // loaded up front (independent loads), then each lane c' < 8 runs the short forward substitution
+  if (lane < 8) {
+    const int cp = lane;
+    double T[8][8];
+#pragma unroll
+    for (int cc = 1; cc < 8; ++cc)
+#pragma unroll
+      for (int c2 = 0; c2 < cc; ++c2) T[cc][c2] = cc < c ? sh.L[buf][8 * P + cc][c2] : 0.0;
+    double w[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      double sacc = (cc == cp) ? 1.0 : 0.0;
+#pragma unroll
+      for (int c2 = 0; c2 < cc; ++c2) sacc = fma(T[cc][c2], w[c2], sacc);
+      w[cc] = sacc;
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) sh.W[buf][cc][cp] = w[cc];
+  }
+  __syncwarp();
 }
 
 // Panel factorization with the full partial-pivoting search (warp argmax per column); rows in natural order.
@@ -436,7 +455,7 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
 #pragma unroll
         for (int w = 0; w < NW; ++w) ju += sh.rowred[w][r];
         double fi = 0.0;
-#pragma unroll 1
+#pragma unroll 4
         for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + r]), fi);
         const double h = p.first ? 0.0 : Jb[int64_t(N) * N + r];
         rhs = fi - 0.5 * ju - 0.5 * nu * h;

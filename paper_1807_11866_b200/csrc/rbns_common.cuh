@@ -8,6 +8,18 @@
 
 namespace rbns {
 
+#ifdef RBNS_TRACE
+__device__ unsigned long long g_trace[256];
+#define RBNS_TR(slot)                                                               \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_trace[(slot) & 255] = clock64(); \
+  } while (0)
+#else
+#define RBNS_TR(slot) \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int kStatusActive = 127;  // internal: sample still iterating
 
 struct ThetaDesc {

@@ -34,6 +34,7 @@ struct ContractParams {
   int32_t N, Ne, Q;       // Ne = κ stride per term (N rounded up to a multiple of 4)
   int32_t nchunks;        // TMA stages per row tile (8 κ each)
   int32_t nsub;           // k4 sub-steps per row tile (= K / 4)
+  int32_t sub_begin;      // first k4 sub-step (Q·Ne/4 at u = 0: only the ν θ_q A_q block is non-zero)
   int32_t row_tiles;      // ceil(R / BN)
   int32_t tiles_per_group;
   int32_t ldu_s;          // shared-memory row stride of the u tile (≡ 8 mod 16)
@@ -43,7 +44,16 @@ struct ContractParams {
   ThetaDesc th;
 };
 
-constexpr int kBM = 64, kBN = 128, kWM = 2, kWN = 4;
+#ifndef RBNS_BN
+#define RBNS_BN 128
+#endif
+#ifndef RBNS_CONTRACT_SCALE_A
+#define RBNS_CONTRACT_SCALE_A 0
+#endif
+#ifndef RBNS_CONTRACT_MINB
+#define RBNS_CONTRACT_MINB 1
+#endif
+constexpr int kBM = 64, kBN = RBNS_BN, kWM = 2, kWN = 4;
 constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 
 // u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups
@@ -54,8 +64,13 @@ __host__ inline size_t contract_smem_bytes(int stages, int ldu, int q) {
          2 * size_t(q) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
 }
 
+#ifdef RBNS_CONTRACT_MAXNREG
+#define RBNS_CONTRACT_BOUNDS(T) __maxnreg__(RBNS_CONTRACT_MAXNREG)
+#else
+#define RBNS_CONTRACT_BOUNDS(T) __launch_bounds__(T, RBNS_CONTRACT_MINB)
+#endif
 template <int BM, int BN, int WM, int WN>
-__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+__global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
     contract_kernel(const __grid_constant__ CUtensorMap tmap, const ContractParams p) {
   constexpr int NCW = WM * WN;
   constexpr int TM = BM / WM, TN = BN / WN;
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     const int b = idx / p.ldu_s, k = idx - b * p.ldu_s;
     const int i = tile0 + b;
     double v = 0.0;
-    if (i < p.n && k < p.N) v = p.u[int64_t(p.act ? p.act[i] : i) * p.N + k];
+    if (i < p.n && k < p.N && p.sub_begin == 0) v = p.u[int64_t(p.act ? p.act[i] : i) * p.N + k];
     Us[idx] = v;
   }
   for (int b = threadIdx.x; b < BM; b += blockDim.x) {
@@ -118,7 +133,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int rt = rt_begin; rt < rt_end; ++rt) {
-        for (int c = 0; c < p.nchunks; ++c) {
+        for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], STAGE * sizeof(double));
           double* dst = Sst + size_t(stage) * STAGE;
@@ -143,6 +158,58 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
   uint32_t phase = 0;
 
   for (int rt = rt_begin; rt < rt_end; ++rt) {
+#if RBNS_CONTRACT_SCALE_A
+    // θ applied to the A fragments (one DMUL per fragment): a single accumulator set, fewer registers
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    int q = 0, k0 = 0;
+    double thq[MI];
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) thq[mi] = thS[sb0 + mi * 8 + g];
+    for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
+      mbar_wait(&full[stage], phase);
+      const double* st = Sst + size_t(stage) * STAGE;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int kap = 8 * c + 4 * j;
+        if (kap >= 4 * p.nsub) break;
+        if (kap < 4 * p.sub_begin) continue;
+        double af[MI], bf[NI];
+        if (kap < kterms) {
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = thq[mi] * Us[(sb0 + mi * 8 + g) * p.ldu_s + k0 + t];
+          k0 += 4;
+          if (k0 == p.Ne) {
+            k0 = 0;
+            ++q;
+            if (q < p.Q) {
+#pragma unroll
+              for (int mi = 0; mi < MI; ++mi) thq[mi] = thS[q * BM + sb0 + mi * 8 + g];
+            }
+          }
+        } else {
+          const int lin = kap - kterms + t;
+#pragma unroll
+          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Q ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
+        }
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) bf[ni] = st[(j * BN + rb0 + ni * 8 + g) * 4 + t];
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == p.stages) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+#else
     double acc[MI][NI][2], accq[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
@@ -150,13 +217,14 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
       for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
 
     int q = 0, k0 = 0;  // current term and k offset of the sub-step (uniform over the warp)
-    for (int c = 0; c < p.nchunks; ++c) {
+    for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
       mbar_wait(&full[stage], phase);
       const double* st = Sst + size_t(stage) * STAGE;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int kap = 8 * c + 4 * j;
         if (kap >= 4 * p.nsub) break;
+        if (kap < 4 * p.sub_begin) continue;
         double af[MI], bf[NI];
         if (kap < kterms) {
 #pragma unroll
@@ -203,6 +271,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         phase ^= 1u;
       }
     }
+#endif
     // epilogue: fragment (sample g, rows 2t..2t+1) -> out[sample][row] as 16-byte stores
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {

@@ -28,7 +28,15 @@ const Shape kShapes[] = {
     {16, 16, 8, 8, newton_gj_kernel<16, 16, 8, 8>},   // N ≤ 127  (8 warps)
 };
 
+// RBNS_GJ_WIDE=1: 8 warps (16×16 grid, 49 register doubles per thread, two CTAs per SM) for 52 < N ≤ 112
+const Shape kWide = {16, 16, 7, 7, newton_gj_kernel<16, 16, 7, 7>};
+
 const Shape* plan(int N) {
+  static const bool wide = [] {
+    const char* v = std::getenv("RBNS_GJ_WIDE");
+    return v && v[0] == '1';
+  }();
+  if (wide && N > 52 && N <= 111) return &kWide;
   for (const Shape& s : kShapes)
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
   return nullptr;
@@ -92,7 +100,13 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (!s) return cudaErrorInvalidValue;
+#ifdef RBNS_GJ_ONE_CTA_PER_SM  // development experiment: force one CTA per SM through unused shared memory
+  static bool set1 = false;
+  if (!set1) { cudaFuncSetAttribute(s->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024); set1 = true; }
+  s->kern<<<p.n, s->tgr * s->tgc, 150 * 1024, st>>>(p);
+#else
   s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
+#endif
   return cudaGetLastError();
 }
 

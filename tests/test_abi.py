@@ -71,4 +71,4 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_native.ThetaTermC) == 24
     assert ctypes.sizeof(_native.ModelDescC) == 16 + 6 * 8
-    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 32
+    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 40
