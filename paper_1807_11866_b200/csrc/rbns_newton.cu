@@ -7,6 +7,7 @@
 
 #include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
+#include "rbns_newton2.cuh"
 #include "rbns_newton_cluster.cuh"
 
 namespace rbns {
@@ -20,12 +21,21 @@ struct Shape {
 };
 
 const Shape kShapes[] = {
-    {4, 8, 4, 3, newton_gj_kernel<4, 8, 4, 3>},       // N ≤ 16   (1 warp)
-    {4, 8, 8, 5, newton_gj_kernel<4, 8, 8, 5>},       // N ≤ 32   (1 warp)
-    {4, 8, 13, 7, newton_gj_kernel<4, 8, 13, 7>},     // N ≤ 52   (1 warp)
-    {8, 16, 10, 6, newton_gj_kernel<8, 16, 10, 6>},   // N ≤ 80   (4 warps)
-    {8, 16, 13, 7, newton_gj_kernel<8, 16, 13, 7>},   // N ≤ 104  (4 warps)
-    {16, 16, 8, 8, newton_gj_kernel<16, 16, 8, 8>},   // N ≤ 127  (8 warps)
+    {4, 8, 4, 3, newton_gj2_kernel<4, 8, 4, 3>},       // N ≤ 16   (1 warp)
+    {4, 8, 8, 5, newton_gj2_kernel<4, 8, 8, 5>},       // N ≤ 32   (1 warp)
+    {4, 8, 13, 7, newton_gj2_kernel<4, 8, 13, 7>},     // N ≤ 52   (1 warp)
+    {8, 16, 10, 6, newton_gj2_kernel<8, 16, 10, 6>},   // N ≤ 80   (4 warps)
+    {8, 16, 13, 7, newton_gj2_kernel<8, 16, 13, 7>},   // N ≤ 104  (4 warps)
+    {16, 16, 8, 8, newton_gj2_kernel<16, 16, 8, 8>},   // N ≤ 127  (8 warps)
+};
+// RBNS_NEWTON=gj1: the earlier owner-serial pivot search (rbns_newton.cuh), kept for comparison
+const Shape kShapes1[] = {
+    {4, 8, 4, 3, newton_gj_kernel<4, 8, 4, 3>},
+    {4, 8, 8, 5, newton_gj_kernel<4, 8, 8, 5>},
+    {4, 8, 13, 7, newton_gj_kernel<4, 8, 13, 7>},
+    {8, 16, 10, 6, newton_gj_kernel<8, 16, 10, 6>},
+    {8, 16, 13, 7, newton_gj_kernel<8, 16, 13, 7>},
+    {16, 16, 8, 8, newton_gj_kernel<16, 16, 8, 8>},
 };
 
 // RBNS_GJ_WIDE=1: 8 warps (16×16 grid, 49 register doubles per thread, two CTAs per SM) for 52 < N ≤ 112
@@ -37,6 +47,14 @@ const Shape* plan(int N) {
     return v && v[0] == '1';
   }();
   if (wide && N > 52 && N <= 111) return &kWide;
+  static const bool v1 = [] {
+    const char* v = std::getenv("RBNS_NEWTON");
+    return v && std::strcmp(v, "gj1") == 0;
+  }();
+  if (v1) {
+    for (const Shape& s : kShapes1)
+      if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
+  }
   for (const Shape& s : kShapes)
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
   return nullptr;

@@ -60,15 +60,20 @@ struct GJShared {
 
 // Pivot-row publication: thread-row tp copies its slot rp (runtime) into P; the recursion keeps register
 // indices static.
-template <int RS, int CS, int SB, int STRIDE, int R = 0>
+// Pivot-row publication: the thread-row holding row slot rp stores a[rp][SB..CS) to P (stride STRIDE).  rp is
+// a runtime value and a[][] lives in registers, so select the slot by a binary search over [LO, HI) (static
+// register indices in every leaf, ⌈log2 RS⌉ branches).
+template <int RS, int CS, int SB, int STRIDE, int LO = 0, int HI = RS>
 __device__ __forceinline__ void publish_row(const double (&a)[RS][CS], int rp, double* P) {
-  if constexpr (R < RS) {
-    if (rp == R) {
+  if constexpr (HI - LO == 1) {
 #pragma unroll
-      for (int s = SB; s < CS; ++s) P[s * STRIDE] = a[R][s];
-    } else {
-      publish_row<RS, CS, SB, STRIDE, R + 1>(a, rp, P);
-    }
+    for (int s = SB; s < CS; ++s) P[s * STRIDE] = a[LO][s];
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    if (rp < MID)
+      publish_row<RS, CS, SB, STRIDE, LO, MID>(a, rp, P);
+    else
+      publish_row<RS, CS, SB, STRIDE, MID, HI>(a, rp, P);
   }
 }
 
