@@ -47,16 +47,16 @@ const Shape* plan(int N) {
     return v && v[0] == '1';
   }();
   if (wide && N > 52 && N <= 111) return &kWide;
-  static const bool v1 = [] {
+  static const int variant = [] {
     const char* v = std::getenv("RBNS_NEWTON");
-    return v && std::strcmp(v, "gj1") == 0;
+    if (v && std::strcmp(v, "gj1") == 0) return 1;
+    return 2;
   }();
-  if (v1) {
-    for (const Shape& s : kShapes1)
-      if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
-  }
-  for (const Shape& s : kShapes)
+  const Shape* table = variant == 1 ? kShapes1 : kShapes;
+  for (int i = 0; i < int(sizeof(kShapes) / sizeof(kShapes[0])); ++i) {
+    const Shape& s = table[i];
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
+  }
   return nullptr;
 }
 

@@ -48,7 +48,9 @@ struct GJ2Shared {
   int sing;
 };
 
-template <int TGR, int TGC, int RS, int CS, int SB>
+// MODE (development ablations, tools/lu_probe.cu; results are wrong for MODE != 0): bit 0 skips the update
+// FMAs, bit 1 skips the pivot search (p = k), bit 2 skips the pivot-row publication.
+template <int TGR, int TGC, int RS, int CS, int SB, int MODE = 0>
 __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const int N, const int tr, const int tc,
                                           GJ2Shared<TGR, TGC, RS, CS>& sh) {
   constexpr int NT = TGR * TGC;
@@ -70,7 +72,7 @@ __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const
       }
       __syncthreads();
       // B: one row per thread, warp argmax on (high word, low word, row)
-      {
+      if constexpr (!(MODE & 2)) {
         unsigned bhi = 0, blo = 0;
         int brow = 0x7fffffff;
         double bval = 0.0;
@@ -106,11 +108,16 @@ __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const
           sh.cand[warp].val = wval;
         }
       }
-      __syncthreads();
+      if constexpr (!(MODE & 2)) __syncthreads();
       // C: reduce the warp winners, publish the pivot row
       unsigned long long bkey = 0;
       int p = 0x7fffffff;
       double piv = 0.0;
+      if constexpr (MODE & 2) {
+        p = k;
+        piv = sh.col[buf][k];
+        bkey = 1;
+      } else
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
         const unsigned long long key = sh.cand[w].key;
@@ -129,7 +136,8 @@ __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const
       const double rpiv = fabs(piv) >= 2.2250738585072014e-308 ? rcp_nr(piv) : 1.0 / piv;
       if (tid == p % NT) sh.col[buf][p] = 0.0;  // the row's searcher (it read row p in B): pivot row not updated
       const int tp = p % TGR, rp = p / TGR;
-      if (tr == tp) publish_row<RS, CS, SB, TGC>(a, rp, &sh.P[0][tc]);
+      if constexpr (!(MODE & 4))
+        if (tr == tp) publish_row<RS, CS, SB, TGC>(a, rp, &sh.P[0][tc]);
       __syncthreads();
       // D: rank-1 update (the pivot row itself: l = 0)
       if (tid == 0) {
@@ -140,30 +148,30 @@ __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const
       double pj[CS];
 #pragma unroll
       for (int s = SB; s < CS; ++s) pj[s] = sh.P[s][tc];
+      if constexpr (!(MODE & 1)) {
 #pragma unroll
-      for (int r = 0; r < RS; ++r) {
-        const double l = sh.col[buf][tr + TGR * r] * rpiv;
+        for (int r = 0; r < RS; ++r) {
+          const double l = sh.col[buf][tr + TGR * r] * rpiv;
 #pragma unroll
-        for (int s = SB; s < CS; ++s) a[r][s] = fma(-l, pj[s], a[r][s]);
+          for (int s = SB; s < CS; ++s) a[r][s] = fma(-l, pj[s], a[r][s]);
+        }
+      } else {
+        a[0][SB] += pj[SB] * rpiv;  // keep the loads alive
       }
     }
-    gj2_block<TGR, TGC, RS, CS, SB + 1>(a, sing, N, tr, tc, sh);
+    gj2_block<TGR, TGC, RS, CS, SB + 1, MODE>(a, sing, N, tr, tc, sh);
   }
 }
 
-template <int TGR, int TGC, int RS, int CS>
-__global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_gj2_kernel(const NewtonParams p) {
+// Kernel prologue shared by the register Gauss–Jordan variants: θ(μ), ν, the J tile into registers and the
+// right-hand side −R = f − ½ J u − ½ ν A(μ)u as column N.  SH needs th, nu, pivoted, rowred, rhs.
+template <int TGR, int TGC, int RS, int CS, class SH>
+__device__ __forceinline__ void gj_load_system(const NewtonParams& p, int i_s, int b, double (&a)[RS][CS], SH& sh) {
   constexpr int NT = TGR * TGC;
-  constexpr int NW = GJ2Shared<TGR, TGC, RS, CS>::NW;
+  constexpr int NW = (NT + 31) / 32;
   constexpr int NR = TGR * RS;
-  static_assert(RS <= 32 && TGR <= 32 && TGC <= 32 && NT % 32 == 0, "shape");
-  __shared__ GJ2Shared<TGR, TGC, RS, CS> sh;
-  const int i_s = blockIdx.x;
-  if (i_s >= p.n) return;
-  const int b = p.act[i_s];
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
-
   if (tid == 0) {
     const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
     sh.nu = 1.0 / re;
@@ -172,8 +180,6 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
   for (int r = tid; r < NR; r += NT) sh.pivoted[r] = 0;
   __syncthreads();
   const double nu = sh.nu;
-
-  double a[RS][CS];
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
 #pragma unroll
   for (int r = 0; r < RS; ++r)
@@ -182,51 +188,53 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
       const int i = tr + TGR * r, j = tc + TGC * s;
       a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
     }
-
-  // right-hand side −R = f − ½ J u − ½ ν A(μ)u, stored as column N
-  {
-    double uj[CS];
+  double uj[CS];
 #pragma unroll
-    for (int s = 0; s < CS; ++s) {
-      const int j = tc + TGC * s;
-      uj[s] = j < N ? p.u[int64_t(b) * N + j] : 0.0;
-    }
-    const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-    for (int r = 0; r < RS; ++r) {
-      double part = 0.0;
-#pragma unroll
-      for (int s = 0; s < CS; ++s) part = fma(a[r][s], uj[s], part);
-#pragma unroll
-      for (int o = TGR; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane < TGR) sh.rowred[warp][tr + TGR * r] = part;
-    }
-    __syncthreads();
-    for (int i = tid; i < NR; i += NT) {
-      double rhs = 0.0;
-      if (i < N) {
-        double ju = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) ju += sh.rowred[w][i];
-        double fi = 0.0;
-#pragma unroll 4
-        for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
-        rhs = fi - 0.5 * ju - 0.5 * nu * Jb[int64_t(N) * N + i];
-      }
-      sh.rhs[i] = rhs;
-    }
-    __syncthreads();
-    if (tc == N % TGC) {
-#pragma unroll
-      for (int r = 0; r < RS; ++r)
-#pragma unroll
-        for (int s = 0; s < CS; ++s)
-          if (tc + TGC * s == N) a[r][s] = sh.rhs[tr + TGR * r];
-    }
+  for (int s = 0; s < CS; ++s) {
+    const int j = tc + TGC * s;
+    uj[s] = j < N ? p.u[int64_t(b) * N + j] : 0.0;
   }
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    double part = 0.0;
+#pragma unroll
+    for (int s = 0; s < CS; ++s) part = fma(a[r][s], uj[s], part);
+#pragma unroll
+    for (int o = TGR; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane < TGR) sh.rowred[warp][tr + TGR * r] = part;
+  }
+  __syncthreads();
+  for (int i = tid; i < NR; i += NT) {
+    double rhs = 0.0;
+    if (i < N) {
+      double ju = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) ju += sh.rowred[w][i];
+      double fi = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
+      rhs = fi - 0.5 * ju - 0.5 * nu * Jb[int64_t(N) * N + i];
+    }
+    sh.rhs[i] = rhs;
+  }
+  __syncthreads();
+  if (tc == N % TGC) {
+#pragma unroll
+    for (int r = 0; r < RS; ++r)
+#pragma unroll
+      for (int s = 0; s < CS; ++s)
+        if (tc + TGC * s == N) a[r][s] = sh.rhs[tr + TGR * r];
+  }
+}
 
-  bool sing = false;
-  gj2_block<TGR, TGC, RS, CS, 0>(a, sing, N, tr, tc, sh);
+// Kernel epilogue: x_k = rhs'[perm k] / piv_k, u += x, ‖δ‖ / ‖u‖ stop rule, per-sample status.
+// SH needs rhs, perm, piv, red.
+template <int TGR, int TGC, int RS, int CS, class SH>
+__device__ __forceinline__ void gj_finish(const NewtonParams& p, int b, const double (&a)[RS][CS], bool sing, SH& sh) {
+  constexpr int NT = TGR * TGC;
+  const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
+  const int N = p.N;
   __syncthreads();
   if (!sing && tc == N % TGC) {
 #pragma unroll
@@ -236,7 +244,6 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
         if (tc + TGC * s == N) sh.rhs[tr + TGR * r] = a[r][s];
   }
   __syncthreads();
-
   double d2 = 0.0, un2 = 0.0;
   if (!sing) {
     for (int k = tid; k < N; k += NT) {
@@ -271,6 +278,21 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
     p.iters[b] = p.iter;
     if (!sing && finite) p.last[b] = sqrt(d2);
   }
+}
+
+template <int TGR, int TGC, int RS, int CS, int MODE = 0>
+__global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_gj2_kernel(const NewtonParams p) {
+  static_assert(RS <= 32 && TGR <= 32 && TGC <= 32 && (TGR * TGC) % 32 == 0, "shape");
+  __shared__ GJ2Shared<TGR, TGC, RS, CS> sh;
+  const int i_s = blockIdx.x;
+  if (i_s >= p.n) return;
+  const int b = p.act[i_s];
+  const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
+  double a[RS][CS];
+  gj_load_system<TGR, TGC, RS, CS>(p, i_s, b, a, sh);
+  bool sing = false;
+  gj2_block<TGR, TGC, RS, CS, 0, MODE>(a, sing, p.N, tr, tc, sh);
+  gj_finish<TGR, TGC, RS, CS>(p, b, a, sing, sh);
 }
 
 }  // namespace rbns

@@ -1,0 +1,84 @@
+// Isolated timing of the Newton-update (Gauss–Jordan) kernels on a random batch, plus gj2 phase ablations
+// (MODE bits: 1 no update, 2 no search, 4 no row publication).  Development tool, not part of the library.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -Ipaper_1807_11866_b200/csrc \
+//        tools/lu_probe.cu -o tools/lu_probe
+#include <cstdio>
+#include <vector>
+
+#include "rbns_newton.cuh"
+#include "rbns_newton2.cuh"
+
+using namespace rbns;
+
+__global__ void fill(double* x, size_t n, unsigned seed) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    unsigned h = unsigned(i) * 2654435761u ^ seed;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+    x[i] = (double(h) / 4294967296.0) * 2.0 - 1.0;
+  }
+}
+
+using K = void (*)(const NewtonParams);
+
+int main(int argc, char** argv) {
+  const int N = argc > 1 ? atoi(argv[1]) : 100;
+  const int B = argc > 2 ? atoi(argv[2]) : 8192;
+  const int64_t ldj = int64_t(N) * N + N;
+  double *J, *u, *mu, *f, *last;
+  int32_t *act, *iters;
+  int8_t* status;
+  cudaMalloc(&J, sizeof(double) * ldj * B);
+  cudaMalloc(&u, sizeof(double) * N * B);
+  cudaMalloc(&mu, sizeof(double) * 2 * B);
+  cudaMalloc(&f, sizeof(double) * N);
+  cudaMalloc(&last, sizeof(double) * B);
+  cudaMalloc(&act, sizeof(int32_t) * B);
+  cudaMalloc(&iters, sizeof(int32_t) * B);
+  cudaMalloc(&status, B);
+  fill<<<1024, 256>>>(J, size_t(ldj) * B, 1u);
+  fill<<<64, 256>>>(f, N, 2u);
+  cudaMemset(u, 0, sizeof(double) * N * B);
+  std::vector<int32_t> h(B);
+  std::vector<double> hm(2 * B);
+  for (int i = 0; i < B; ++i) { h[i] = i; hm[2 * i] = 0.3; hm[2 * i + 1] = 100.0; }
+  cudaMemcpy(act, h.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice);
+  cudaMemcpy(mu, hm.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice);
+  NewtonParams p{};
+  p.act = act; p.n = B; p.J = J; p.ldj = ldj; p.u = u; p.mu = mu; p.A = nullptr; p.f = f;
+  p.N = N; p.Q = 1; p.first = 0; p.iter = 1; p.max_iter = 100; p.tol = 1e-12;
+  p.iters = iters; p.status = status; p.last = last;
+  p.th.q = 1; p.th.kind[0] = RBNS_THETA_CONST; p.th.scale[0] = 1.0;
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  struct V { const char* name; K k; int threads; };
+  const V vs[] = {
+      {"gj1", newton_gj_kernel<8, 16, 13, 7>, 128},
+      {"gj2", newton_gj2_kernel<8, 16, 13, 7, 0>, 128},
+      {"gj2 -update", newton_gj2_kernel<8, 16, 13, 7, 1>, 128},
+      {"gj2 -search", newton_gj2_kernel<8, 16, 13, 7, 2>, 128},
+      {"gj2 -publish", newton_gj2_kernel<8, 16, 13, 7, 4>, 128},
+      {"gj2 -update-search", newton_gj2_kernel<8, 16, 13, 7, 3>, 128},
+      {"gj2 -all", newton_gj2_kernel<8, 16, 13, 7, 7>, 128},
+  };
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (const V& v : vs) {
+    v.k<<<B, v.threads>>>(p);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) v.k<<<B, v.threads>>>(p);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    // SM-clocks per (sample, elimination step): how long one SM spends per step of one sample
+    const double clk = double(ms) * 1e-3 * clk_khz * 1e3 * sms / (double(B) * N);
+    printf("%-22s %8.3f ms  %7.1f SM-clk per sample-step  (x2 CTAs/SM: %6.0f clk per CTA step)  %s\n", v.name, ms,
+           clk, 2 * clk, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}

@@ -1,9 +1,11 @@
 #!/bin/bash
-# One GPU session: bench line, plain run + ncu launch list of one bench step, full ncu capture of the two hot kernels.
+# One GPU session: bench line (+ reference arm), plain run + ncu launch list of one bench step, full ncu capture
+# of the two hot kernels (contraction + Newton update) on a fixed cfg-2 workload.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
