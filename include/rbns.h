@@ -6,6 +6,9 @@
  * module.  Each entry point names the SPEC operation it replaces:
  *
  *   rbns_model_create        <- ReducedModel hand-off to the online stage
+ *   rbns_model_create2       <- same, per-form term families (a/c0 linear, c quadratic, d0/f loads, B
+ *                               coupling) with their own descriptors (SPEC.md:339-346 AffineFormSet,
+ *                               SPEC.md:449-457 build_reduced_model)
  *   rbns_solve               <- online.solve_block, batched ("batch sweep API")
  *   rbns_solve_host          <- same, host buffers in/out (the query API a CPU caller binds)
  *   rbns_reduced_operator    <- online.reduced_operator (residual + Jacobian)
@@ -27,16 +30,18 @@
 extern "C" {
 #endif
 
-#define RBNS_ABI_VERSION 1
-#define RBNS_MAX_TERMS 16
+#define RBNS_ABI_VERSION 2
+#define RBNS_MAX_TERMS 128 /* per term family */
+#define RBNS_MAX_GROUPS 4  /* distinct mu1 powers tying linear terms to the quadratic blocks (see create2) */
 
-/* θ_q(μ) descriptor kinds; μ = (alpha [rad], Re).  value = scale * base. */
+/* θ_q(μ) descriptor kinds; μ = (mu0, mu1) = (alpha [rad], Re) for the BASELINE configs, (φ [rad], u∞) for the
+ * paper's models.  value = scale * base. */
 enum rbns_theta_kind {
   RBNS_THETA_CONST = 0,       /* 1                           */
   RBNS_THETA_COS_K = 1,       /* cos(k alpha)                */
   RBNS_THETA_SIN_K = 2,       /* sin(k alpha)                */
   RBNS_THETA_COS_SIN_POW = 3, /* cos(alpha)^k * sin(alpha)^m */
-  RBNS_THETA_MONOMIAL = 4     /* alpha^k * Re^m  (the paper's scale*phi^k*u_inf^m) */
+  RBNS_THETA_MONOMIAL = 4     /* mu0^k * mu1^m  (the paper's scale*phi^k*u_inf^m) */
 };
 
 /* per-sample outcome (int8) */
@@ -78,6 +83,39 @@ typedef struct rbns_model_desc {
   const rbns_theta_term* theta; /* host, Q descriptors                                      */
 } rbns_model_desc;
 
+/* One affine family: count terms, each an operator of the family's shape with its own descriptor. */
+typedef struct rbns_term_family {
+  int32_t count;                /* 0..RBNS_MAX_TERMS                                        */
+  int32_t reserved;
+  const double* data;           /* host, count x (family shape), row-major                 */
+  const rbns_theta_term* theta; /* host, count descriptors                                  */
+} rbns_term_family;
+
+enum rbns_model_flags {
+  RBNS_NU_LINEAR = 1 /* multiply the linear family by nu = 1/mu1 (BASELINE configs); clear for the paper's
+                        models, whose a-term descriptors carry nu in their scale */
+};
+
+/* Reduced model with per-form families.  Residual and Jacobian:
+ *   R(u) = L(mu) u + sum_c theta_c(mu) C_c(u, u) - sum_f theta_f(mu) f_f
+ *   J(u) = L(mu)   + sum_c theta_c(mu) sum_k (C_c[m,k,l] + C_c[k,m,l]) u_k
+ *   L(mu) = [nu] sum_a theta_a(mu) A_a        (a-terms and the lift's c0-terms: everything linear in u)
+ * Pressure recovery (cfg-4 form): Mp p = sum_b theta_b(mu) B_b u.
+ * Each linear term's h-row contribution (L u, needed by the residual) rides on the quadratic block whose
+ * descriptor equals its own up to a constant factor and a power of mu1 (RBNS_MAX_GROUPS distinct powers);
+ * linear terms without such a block get an extra (velocity-free) block of the contraction. */
+typedef struct rbns_model_desc2 {
+  int32_t n;                   /* reduced velocity dimension N                           */
+  int32_t n_p;                 /* pressure dimension Np (0 = no recovery)                */
+  int32_t flags;               /* rbns_model_flags                                       */
+  int32_t reserved;
+  rbns_term_family linear;     /* count x N x N         (>= 1 term)                      */
+  rbns_term_family quadratic;  /* count x N x N x N     C[j][k][l] = c(u_j, u_k, u_l)    */
+  rbns_term_family load;       /* count x N                                              */
+  rbns_term_family coupling;   /* count x Np x N        (Np > 0)                         */
+  const double* Mp;            /* host Np x Np SPD, or NULL when Np = 0                  */
+} rbns_model_desc2;
+
 typedef struct rbns_model rbns_model;
 
 /* Per-call statistics of the last rbns_solve / rbns_solve_host on this model (thread-unsafe read). */
@@ -98,6 +136,11 @@ typedef struct rbns_stats {
 /* Copy operators to `device`, build the symmetrised GEMM operand S_q = C_q + C_q^(12),
  * and factor Mp once.  The handle is immutable afterwards and may be shared by concurrent solves. */
 int rbns_model_create(const rbns_model_desc* desc, int device, rbns_model** out);
+/* Per-family form; rbns_model_create(d) == rbns_model_create2 with every family on d->theta and
+ * RBNS_NU_LINEAR. */
+int rbns_model_create2(const rbns_model_desc2* desc, int device, rbns_model** out);
+/* term counts: linear, quadratic, load, coupling, contraction blocks (quadratic + extra), h groups */
+int rbns_model_terms(const rbns_model* model, int32_t counts[6]);
 int rbns_model_destroy(rbns_model* model);
 int rbns_model_info(const rbns_model* model, int32_t* n, int32_t* q, int32_t* n_p, int32_t* device);
 /* bytes of device memory the handle owns */

@@ -14,12 +14,14 @@ from .errors import NativeError
 
 LIB_PATH = Path(os.environ.get("RBNS_LIB", Path(__file__).resolve().parent / "librbns.so"))
 
-MAX_TERMS = 16
+MAX_TERMS = 128
+MAX_GROUPS = 4
+NU_LINEAR = 1
 STATUS_NAMES = {0: "CONVERGED", 1: "NON_CONVERGED", 2: "SINGULAR_SYSTEM", 3: "SINGULAR_RECOVERY", 4: "NONFINITE"}
 
 # every symbol include/rbns.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (
-    "rbns_model_create", "rbns_model_destroy", "rbns_model_info", "rbns_model_device_bytes", "rbns_solve",
+    "rbns_model_create", "rbns_model_create2", "rbns_model_terms", "rbns_model_destroy", "rbns_model_info", "rbns_model_device_bytes", "rbns_solve",
     "rbns_solve_host", "rbns_reduced_operator", "rbns_recover_pressure", "rbns_get_stats",
     "rbns_error_string", "rbns_last_error_message", "rbns_abi_version",
 )
@@ -35,6 +37,17 @@ class ModelDescC(ctypes.Structure):
                 ("reserved", ctypes.c_int32),
                 ("A", ctypes.c_void_p), ("C", ctypes.c_void_p), ("f", ctypes.c_void_p),
                 ("Mp", ctypes.c_void_p), ("Bq", ctypes.c_void_p), ("theta", ctypes.POINTER(ThetaTermC))]
+
+
+class TermFamilyC(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int32), ("reserved", ctypes.c_int32), ("data", ctypes.c_void_p),
+                ("theta", ctypes.POINTER(ThetaTermC))]
+
+
+class ModelDesc2C(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("n_p", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("linear", TermFamilyC), ("quadratic", TermFamilyC),
+                ("load", TermFamilyC), ("coupling", TermFamilyC), ("Mp", ctypes.c_void_p)]
 
 
 class StatsC(ctypes.Structure):
@@ -66,6 +79,8 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
         raise NativeError(f"failed to load {p}: {exc}") from exc
     vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     lib.rbns_model_create.argtypes = [ctypes.POINTER(ModelDescC), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.rbns_model_create2.argtypes = [ctypes.POINTER(ModelDesc2C), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.rbns_model_terms.argtypes = [vp, ctypes.POINTER(i32)]
     lib.rbns_model_destroy.argtypes = [vp]
     lib.rbns_model_info.argtypes = [vp] + [ctypes.POINTER(i32)] * 4
     lib.rbns_model_device_bytes.argtypes = [vp]

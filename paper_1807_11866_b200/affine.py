@@ -6,7 +6,8 @@ Reference: ``CoefficientDescriptor`` ("evaluation is exactly sc
 expressed here as a list of :class:`ThetaTerm` descriptors whose evaluation rule is shared, term by term, with
 the CUDA kernels (``csrc/rbns_common.cuh: eval_theta``) so the host and the device evaluate θ identically.
 
-μ is always ``(alpha [rad], Re)``; the viscosity rule is ν = 1/Re (BASELINE.json config 0).
+μ is ``(alpha [rad], Re)`` for the BASELINE configs (viscosity rule ν = 1/Re, BASELINE.json config 0) and
+``(φ [rad], u∞)`` for the paper's lifted models, whose descriptors carry ν themselves.
 """
 
 from __future__ import annotations
@@ -23,7 +24,7 @@ SIN_K = 2          # scale * sin(k α)
 COS_SIN_POW = 3    # scale * cos(α)^k * sin(α)^m
 MONOMIAL = 4       # scale * α^k * Re^m      (the paper's scale·φᵏ·u∞ᵐ)
 
-MAX_TERMS = 16     # RBNS_MAX_TERMS
+MAX_TERMS = 128    # RBNS_MAX_TERMS (per term family)
 
 
 @dataclass(frozen=True)

@@ -111,22 +111,33 @@ int64_t env_int64(const char* name, int64_t dflt) {
 
 }  // namespace
 
+// One contraction operand: S (rows × kalloc, L2-resident, TMA-streamed) and its weight descriptors.
+struct Operand {
+  CUtensorMap tm{};
+  double* S = nullptr;
+  int64_t rows = 0, row_tiles = 0;
+  int kalloc = 0, nchunks = 0, nsub = 0;
+  int Qb = 0, Ql = 0;                      // θ ⊗ u blocks, affine columns
+  const rbns_theta_term* thb = nullptr;    // device descriptors
+  const rbns_theta_term* thl = nullptr;
+  int stages = 0;
+  size_t smem = 0;
+};
+
 struct rbns_model {
   int device = 0;
   int num_sms = 148;
-  int N = 0, Q = 0, Np = 0, Ne = 0, kalloc = 0, nchunks = 0, nsub = 0;
-  int64_t R = 0, row_tiles = 0, rp_tiles = 0;
-  double* S = nullptr;   // [R][kalloc]
-  double* A = nullptr;   // [Q][N][N]
-  double* f = nullptr;   // [Q][N]
-  double* Sp = nullptr;  // [Np][kalloc]
-  double* L = nullptr;   // [Np][Np]
-  double* Lt = nullptr;  // [Np][Np]
+  int N = 0, Np = 0, Ne = 0, ldu = 0;
+  int Qa = 0, Qc = 0, Qf = 0, Qp = 0;      // family sizes: linear, quadratic, load, coupling
+  int G = 0, ge[RBNS_MAX_GROUPS] = {};     // h groups and their μ₁ exponents
+  int nu_lin = 0;
+  Operand vel, prs;
+  double* f = nullptr;                     // [Qf][N]
+  double* L = nullptr;                     // [Np][Np]
+  double* Lt = nullptr;                    // [Np][Np]
+  rbns_theta_term* dth = nullptr;          // device descriptors: blocks | linear | load | coupling
+  const rbns_theta_term* thf = nullptr;
   int rec_ok = 0;
-  CUtensorMap tmS{}, tmSp{};
-  ThetaDesc th{};
-  int stages = 0, ldu = 0;
-  size_t smem = 0;
   int64_t bytes = 0;
   rbns_stats stats{};
   std::mutex stats_mu;
@@ -140,9 +151,8 @@ namespace {
 using ContractKernel = void (*)(const CUtensorMap, const ContractParams);
 constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN>;
 
-int launch_contract(rbns_model* m, const CUtensorMap& tm, int64_t row_tiles, const int32_t* act, int n,
-                    const double* u, const double* mu, double* out, int64_t ldo, cudaStream_t st,
-                    bool linear_only = false) {
+int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n, const double* u, const double* mu,
+                    double* out, int64_t ldo, cudaStream_t st, bool linear_only = false) {
   if (n <= 0) return RBNS_OK;
   ContractParams p{};
   p.act = act;
@@ -151,51 +161,59 @@ int launch_contract(rbns_model* m, const CUtensorMap& tm, int64_t row_tiles, con
   p.mu = mu;
   p.N = m->N;
   p.Ne = m->Ne;
-  p.Q = m->Q;
-  p.nchunks = m->nchunks;
-  p.nsub = m->nsub;
-  p.sub_begin = linear_only ? (m->Q * m->Ne) / 4 : 0;
-  p.row_tiles = int(row_tiles);
+  p.Qb = op.Qb;
+  p.Ql = op.Ql;
+  p.nu_lin = m->nu_lin;
+  p.thb = op.thb;
+  p.thl = op.thl;
+  p.nchunks = op.nchunks;
+  p.nsub = op.nsub;
+  p.sub_begin = linear_only ? (op.Qb * m->Ne) / 4 : 0;
+  p.row_tiles = int(op.row_tiles);
   p.ldu_s = m->ldu;
-  p.stages = m->stages;
+  p.stages = op.stages;
   p.out = out;
   p.ldo = ldo;
-  p.th = m->th;
   const int sample_tiles = (n + kBM - 1) / kBM;
   const int64_t want = 8LL * m->num_sms;
   int groups = int(std::max<int64_t>(1, (want + sample_tiles - 1) / sample_tiles));
-  groups = int(std::min<int64_t>(groups, std::max<int64_t>(1, (row_tiles + 3) / 4)));
-  p.tiles_per_group = int((row_tiles + groups - 1) / groups);
-  groups = int((row_tiles + p.tiles_per_group - 1) / p.tiles_per_group);
+  groups = int(std::min<int64_t>(groups, std::max<int64_t>(1, (op.row_tiles + 3) / 4)));
+  p.tiles_per_group = int((op.row_tiles + groups - 1) / groups);
+  groups = int((op.row_tiles + p.tiles_per_group - 1) / p.tiles_per_group);
   dim3 grid(sample_tiles, groups);
-  kContract<<<grid, kContractThreads, m->smem, st>>>(tm, p);
+  kContract<<<grid, kContractThreads, op.smem, st>>>(op.tm, p);
   RBNS_CUDA(cudaGetLastError());
   return RBNS_OK;
 }
 
-int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
-                  const double* mu, int first, int iter, int max_iter, double tol, int32_t* iters, int8_t* status,
-                  double* last, cudaStream_t st) {
-  if (n <= 0) return RBNS_OK;
+NewtonParams newton_params(const rbns_model* m) {
   NewtonParams p{};
+  p.f = m->f;
+  p.thf = m->thf;
+  p.N = m->N;
+  p.Qf = m->Qf;
+  p.G = m->G;
+  for (int g = 0; g < RBNS_MAX_GROUPS; ++g) p.ge[g] = m->ge[g];
+  return p;
+}
+
+int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
+                  const double* mu, int iter, int max_iter, double tol, int32_t* iters, int8_t* status, double* last,
+                  cudaStream_t st) {
+  if (n <= 0) return RBNS_OK;
+  NewtonParams p = newton_params(m);
   p.act = act;
   p.n = n;
   p.J = J;
   p.ldj = ldj;
   p.u = u;
   p.mu = mu;
-  p.A = m->A;
-  p.f = m->f;
-  p.N = m->N;
-  p.Q = m->Q;
-  p.first = first;
   p.iter = iter;
   p.max_iter = max_iter;
   p.tol = tol;
   p.iters = iters;
   p.status = status;
   p.last = last;
-  p.th = m->th;
   RBNS_CUDA(launch_newton_update(p, st));
   return RBNS_OK;
 }
@@ -243,7 +261,7 @@ struct Timer {
 int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double* p, int8_t* status, cudaStream_t st,
             rbns_stats& stats) {
   if (!m->Np) return fail(RBNS_ERR_NO_PRESSURE, "model has no pressure-recovery operators");
-  const int64_t ldr = m->rp_tiles * kBN;
+  const int64_t ldr = m->prs.row_tiles * kBN;
   const int64_t budget = env_int64("RBNS_RBUF_BYTES", int64_t(1) << 30);
   const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldr * 8)));
   double* rbuf = nullptr;
@@ -253,7 +271,7 @@ int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double*
   for (int64_t c0 = 0; c0 < B && rc == RBNS_OK; c0 += cap) {
     const int nc = int(std::min<int64_t>(cap, B - c0));
     // identity ids for this chunk: contraction reads u/mu by id = c0 + i via offset pointers
-    rc = launch_contract(m, m->tmSp, m->rp_tiles, nullptr, nc, u + c0 * m->N, mu + 2 * c0, rbuf, ldr, st);
+    rc = launch_contract(m, m->prs, nullptr, nc, u + c0 * m->N, mu + 2 * c0, rbuf, ldr, st);
     if (rc) break;
     stats.kernel_launches += 1;
     const int threads = 256, blocks = int((int64_t(nc) * 32 + threads - 1) / threads);
@@ -287,7 +305,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
   cudaEventCreate(&t1);
   cudaEventRecord(t0, st);
 
-  const int64_t ldj = m->row_tiles * kBN;
+  const int64_t ldj = m->vel.row_tiles * kBN;
   int32_t *act0 = nullptr, *act1 = nullptr, *dcount = nullptr;
   RBNS_CUDA(cudaMallocAsync(&act0, size_t(B) * sizeof(int32_t), st));
   RBNS_CUDA(cudaMallocAsync(&act1, size_t(B) * sizeof(int32_t), st));
@@ -315,17 +333,17 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     for (int64_t c0 = 0; c0 < n_act && rc == RBNS_OK; c0 += csz) {
       const int nc = int(std::min<int64_t>(csz, n_act - c0));
       {
-        // u = 0 at the first step: the convective part vanishes, only the ν θ_q A_q block of the GEMM runs
-        // (J = ν A(μ), h = 0); later steps run the full contraction
+        // u = 0 at the first step: the convective part vanishes, only the affine block of the GEMM runs
+        // (J = L(μ), h = 0); later steps run the full contraction
         const int e = timer.begin(first ? 3 : 0);
-        rc = launch_contract(m, m->tmS, m->row_tiles, act0 + c0, nc, u, mu, jbuf, ldj, st, first);
+        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first);
         timer.end(e);
         if (rc) break;
         stats.gemm_launches += 1;
         stats.kernel_launches += 1;
       }
       const int e = timer.begin(1);
-      rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, 0, it, max_iter, tol, iters, status, last, st);
+      rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, st);
       timer.end(e);
       if (rc) break;
       stats.lu_launches += 1;
@@ -407,17 +425,75 @@ const char* rbns_last_error_message(void) { return g_last_error.c_str(); }
 
 int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
   if (!d || !out) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL descriptor/out");
-  *out = nullptr;
-  if (d->n < 1 || d->q < 1 || d->q > RBNS_MAX_TERMS || d->n_p < 0)
-    return fail(RBNS_ERR_INVALID_ARGUMENT, "need N >= 1, 1 <= Q <= 16, Np >= 0");
-  if (!d->A || !d->C || !d->f || !d->theta) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL operator pointer");
-  if (d->n_p > 0 && (!d->Mp || !d->Bq)) return fail(RBNS_ERR_INVALID_ARGUMENT, "Np > 0 needs Mp and Bq");
-  if (d->n_p > 256) return fail(RBNS_ERR_UNSUPPORTED, "Np > 256");
-  for (int q = 0; q < d->q; ++q) {
-    const auto& t = d->theta[q];
-    if (t.kind < RBNS_THETA_CONST || t.kind > RBNS_THETA_MONOMIAL || t.k < 0 || t.m < 0)
-      return fail(RBNS_ERR_INVALID_ARGUMENT, "bad theta descriptor " + std::to_string(q));
+  rbns_model_desc2 d2{};
+  d2.n = d->n;
+  d2.n_p = d->n_p;
+  d2.flags = RBNS_NU_LINEAR;
+  d2.linear = {d->q, 0, d->A, d->theta};
+  d2.quadratic = {d->q, 0, d->C, d->theta};
+  d2.load = {d->q, 0, d->f, d->theta};
+  d2.coupling = {d->n_p > 0 ? d->q : 0, 0, d->Bq, d->theta};
+  d2.Mp = d->Mp;
+  return rbns_model_create2(&d2, device, out);
+}
+
+namespace {
+
+bool valid_terms(const rbns_term_family& fam, bool need_data, const char* name, std::string& why) {
+  if (fam.count < 0 || fam.count > RBNS_MAX_TERMS) {
+    why = std::string(name) + ": count outside [0, " + std::to_string(RBNS_MAX_TERMS) + "]";
+    return false;
   }
+  if (fam.count > 0 && ((need_data && !fam.data) || !fam.theta)) {
+    why = std::string(name) + ": NULL data/theta";
+    return false;
+  }
+  for (int q = 0; q < fam.count; ++q) {
+    const auto& t = fam.theta[q];
+    if (t.kind < RBNS_THETA_CONST || t.kind > RBNS_THETA_MONOMIAL || t.k < 0 || t.m < 0 || !std::isfinite(t.scale)) {
+      why = std::string(name) + ": bad theta descriptor " + std::to_string(q);
+      return false;
+    }
+  }
+  return true;
+}
+
+// θ_a(μ) == rho · μ₁^e · θ_c(μ) for every μ?  (same base function up to a constant and a power of μ₁)
+bool tie(const rbns_theta_term& a, const rbns_theta_term& c, int& e, double& rho) {
+  if (a.kind != c.kind || c.scale == 0.0) return false;
+  e = 0;
+  switch (a.kind) {
+    case RBNS_THETA_CONST: break;
+    case RBNS_THETA_COS_K:
+    case RBNS_THETA_SIN_K:
+      if (a.k != c.k) return false;
+      break;
+    case RBNS_THETA_COS_SIN_POW:
+      if (a.k != c.k || a.m != c.m) return false;
+      break;
+    default:  // monomial μ₀^k μ₁^m
+      if (a.k != c.k) return false;
+      e = a.m - c.m;
+      break;
+  }
+  rho = a.scale / c.scale;
+  return std::isfinite(rho);
+}
+
+}  // namespace
+
+int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) {
+  if (!d || !out) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL descriptor/out");
+  *out = nullptr;
+  std::string why;
+  if (d->n < 1 || d->n_p < 0) return fail(RBNS_ERR_INVALID_ARGUMENT, "need N >= 1, Np >= 0");
+  if (!valid_terms(d->linear, true, "linear", why) || !valid_terms(d->quadratic, true, "quadratic", why) ||
+      !valid_terms(d->load, true, "load", why) || !valid_terms(d->coupling, true, "coupling", why))
+    return fail(RBNS_ERR_INVALID_ARGUMENT, why);
+  if (d->linear.count < 1) return fail(RBNS_ERR_INVALID_ARGUMENT, "the linear family needs >= 1 term");
+  if (d->n_p > 0 && (!d->Mp || d->coupling.count < 1))
+    return fail(RBNS_ERR_INVALID_ARGUMENT, "Np > 0 needs Mp and >= 1 coupling term");
+  if (d->n_p > 256) return fail(RBNS_ERR_UNSUPPORTED, "Np > 256");
   if (!newton_supported(d->n))
     return fail(RBNS_ERR_UNSUPPORTED, "N=" + std::to_string(d->n) + " exceeds the register-resident Newton kernel");
   int ndev = 0;
@@ -425,39 +501,76 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
   if (device < 0 || device >= ndev) return fail(RBNS_ERR_INVALID_ARGUMENT, "bad device index");
   DeviceGuard guard(device);
 
+  // ---- host planning: tie each linear term's h rows to a contraction block ----
+  const int Qa = d->linear.count, Qc = d->quadratic.count;
+  std::vector<rbns_theta_term> blocks(d->quadratic.theta, d->quadratic.theta + Qc);
+  std::vector<int> hb(Qa), hg(Qa);
+  std::vector<double> rho(Qa);
+  std::vector<int> ge;
+  const int nu_lin = (d->flags & RBNS_NU_LINEAR) ? 1 : 0;
+  for (int a = 0; a < Qa; ++a) {
+    const rbns_theta_term& ta = d->linear.theta[a];
+    int e = 0, j = -1;
+    double r = 1.0;
+    for (int c = 0; c < int(blocks.size()) && j < 0; ++c)
+      if (tie(ta, blocks[c], e, r)) j = c;
+    if (j < 0) {  // no block carries this base function: an extra, velocity-free block
+      if (int(blocks.size()) >= RBNS_MAX_TERMS) return fail(RBNS_ERR_UNSUPPORTED, "too many contraction blocks");
+      blocks.push_back(ta);
+      j = int(blocks.size()) - 1;
+      e = 0;
+      r = 1.0;
+    }
+    e -= nu_lin;  // ν = μ₁⁻¹ on the whole linear family
+    int g = int(std::find(ge.begin(), ge.end(), e) - ge.begin());
+    if (g == int(ge.size())) {
+      if (int(ge.size()) >= RBNS_MAX_GROUPS)
+        return fail(RBNS_ERR_UNSUPPORTED, "linear terms need more than RBNS_MAX_GROUPS distinct mu1 powers");
+      ge.push_back(e);
+    }
+    hb[a] = j;
+    hg[a] = g;
+    rho[a] = r;
+  }
+
   auto m = new rbns_model();
   m->device = device;
   cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
   m->N = d->n;
-  m->Q = d->q;
   m->Np = d->n_p;
-  m->Ne = (m->N + 3) / 4 * 4;                      // κ stride per affine term (k4 sub-steps never straddle)
-  const int K = m->Q * m->Ne + (m->Q + 3) / 4 * 4;  // + the ν θ_q block
-  m->kalloc = K;
-  m->nchunks = (K + 7) / 8;
-  m->nsub = K / 4;
-  m->R = int64_t(m->N) * m->N + m->N;
-  m->row_tiles = (m->R + kBN - 1) / kBN;
-  m->rp_tiles = (m->Np + kBN - 1) / kBN;
-  m->th.q = m->Q;
-  for (int q = 0; q < m->Q; ++q) {
-    m->th.kind[q] = d->theta[q].kind;
-    m->th.k[q] = d->theta[q].k;
-    m->th.m[q] = d->theta[q].m;
-    m->th.scale[q] = d->theta[q].scale;
-  }
+  m->Qa = Qa;
+  m->Qc = Qc;
+  m->Qf = d->load.count;
+  m->Qp = d->n_p > 0 ? d->coupling.count : 0;
+  m->nu_lin = nu_lin;
+  m->G = int(ge.size());
+  for (int g = 0; g < m->G; ++g) m->ge[g] = ge[g];
+  m->Ne = (m->N + 3) / 4 * 4;  // κ stride per block (k4 sub-steps never straddle)
   m->ldu = contract_ldu(m->Ne);
-  int max_smem = 0;
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  m->stages = 16;
-  while (m->stages > 2 && contract_smem_bytes(m->stages, m->ldu, m->Q) > size_t(max_smem)) --m->stages;
-  m->smem = contract_smem_bytes(m->stages, m->ldu, m->Q);
   auto cleanup = [&](int rc) {
     rbns_model_destroy(m);
     return rc;
   };
-  if (m->smem > size_t(max_smem))
-    return cleanup(fail(RBNS_ERR_UNSUPPORTED, "u tile does not fit shared memory for N=" + std::to_string(m->N)));
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  auto plan = [&](Operand& op, int64_t rows, int qb, int ql) {
+    op.rows = rows;
+    op.row_tiles = (rows + kBN - 1) / kBN;
+    op.Qb = qb;
+    op.Ql = ql;
+    op.kalloc = qb * m->Ne + (ql + 3) / 4 * 4;
+    op.nchunks = (op.kalloc + 7) / 8;
+    op.nsub = op.kalloc / 4;
+    op.stages = 16;
+    while (op.stages > 2 && contract_smem_bytes(op.stages, m->ldu, qb, ql) > size_t(max_smem)) --op.stages;
+    op.smem = contract_smem_bytes(op.stages, m->ldu, qb, ql);
+    return op.smem <= size_t(max_smem);
+  };
+  const int Qb = int(blocks.size());
+  if (!plan(m->vel, int64_t(m->N) * m->N + int64_t(m->G) * m->N, Qb, Qa) ||
+      (m->Np && !plan(m->prs, m->Np, m->Qp, 0)))
+    return cleanup(fail(RBNS_ERR_UNSUPPORTED, "contraction tile does not fit shared memory for N=" +
+                                                  std::to_string(m->N)));
   // a per-function cap shared by every model: set it to the device maximum (not this model's size), so a
   // model created later with a smaller tile cannot invalidate launches of an earlier one
   if (cudaFuncSetAttribute(kContract, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) != cudaSuccess)
@@ -470,10 +583,6 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
 
-  const int64_t N = m->N, Q = m->Q;
-  const size_t cbytes = size_t(Q) * N * N * N * sizeof(double);
-  double* dC = nullptr;
-  if (cudaMalloc(&dC, cbytes) != cudaSuccess) return cleanup(fail(RBNS_ERR_OUT_OF_MEMORY, "cudaMalloc(C)"));
   auto step = [&](cudaError_t e, const char* what) {
     if (e != cudaSuccess) {
       fail(e == cudaErrorMemoryAllocation ? RBNS_ERR_OUT_OF_MEMORY : RBNS_ERR_CUDA,
@@ -482,20 +591,54 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
     }
     return true;
   };
-  bool ok = step(cudaMemcpy(dC, d->C, cbytes, cudaMemcpyHostToDevice), "upload C") &&
-            step(cudaMalloc(&m->A, size_t(Q) * N * N * sizeof(double)), "cudaMalloc(A)") &&
-            step(cudaMemcpy(m->A, d->A, size_t(Q) * N * N * sizeof(double), cudaMemcpyHostToDevice), "upload A") &&
-            step(cudaMalloc(&m->f, size_t(Q) * N * sizeof(double)), "cudaMalloc(f)") &&
-            step(cudaMemcpy(m->f, d->f, size_t(Q) * N * sizeof(double), cudaMemcpyHostToDevice), "upload f") &&
-            step(cudaMalloc(&m->S, size_t(m->R) * m->kalloc * sizeof(double)), "cudaMalloc(S)");
+  auto bad = [&]() {
+    return cleanup(g_last_error.find("memory") != std::string::npos ? RBNS_ERR_OUT_OF_MEMORY : RBNS_ERR_CUDA);
+  };
+  // descriptors on the device: blocks | linear | load | coupling
+  std::vector<rbns_theta_term> th(blocks);
+  th.insert(th.end(), d->linear.theta, d->linear.theta + Qa);
+  if (m->Qf) th.insert(th.end(), d->load.theta, d->load.theta + m->Qf);
+  if (m->Qp) th.insert(th.end(), d->coupling.theta, d->coupling.theta + m->Qp);
+  if (!step(cudaMalloc(&m->dth, th.size() * sizeof(rbns_theta_term)), "cudaMalloc(theta)") ||
+      !step(cudaMemcpy(m->dth, th.data(), th.size() * sizeof(rbns_theta_term), cudaMemcpyHostToDevice),
+            "upload theta"))
+    return bad();
+  m->vel.thb = m->dth;
+  m->vel.thl = m->dth + Qb;
+  m->thf = m->dth + Qb + Qa;
+  m->prs.thb = m->dth + Qb + Qa + m->Qf;
+
+  const int64_t N = m->N;
+  double *dC = nullptr, *dA = nullptr, *drho = nullptr;
+  int *dhb = nullptr, *dhg = nullptr;
+  const size_t cbytes = size_t(std::max(Qc, 1)) * N * N * N * sizeof(double);
+  bool ok = step(cudaMalloc(&dC, cbytes), "cudaMalloc(C)") &&
+            (Qc == 0 || step(cudaMemcpy(dC, d->quadratic.data, size_t(Qc) * N * N * N * sizeof(double),
+                                        cudaMemcpyHostToDevice), "upload C")) &&
+            step(cudaMalloc(&dA, size_t(Qa) * N * N * sizeof(double)), "cudaMalloc(A)") &&
+            step(cudaMemcpy(dA, d->linear.data, size_t(Qa) * N * N * sizeof(double), cudaMemcpyHostToDevice),
+                 "upload A") &&
+            step(cudaMalloc(&dhb, Qa * sizeof(int)), "cudaMalloc(hb)") &&
+            step(cudaMalloc(&dhg, Qa * sizeof(int)), "cudaMalloc(hg)") &&
+            step(cudaMalloc(&drho, Qa * sizeof(double)), "cudaMalloc(rho)") &&
+            step(cudaMemcpy(dhb, hb.data(), Qa * sizeof(int), cudaMemcpyHostToDevice), "upload hb") &&
+            step(cudaMemcpy(dhg, hg.data(), Qa * sizeof(int), cudaMemcpyHostToDevice), "upload hg") &&
+            step(cudaMemcpy(drho, rho.data(), Qa * sizeof(double), cudaMemcpyHostToDevice), "upload rho") &&
+            step(cudaMalloc(&m->f, size_t(std::max(m->Qf, 1)) * N * sizeof(double)), "cudaMalloc(f)") &&
+            (m->Qf == 0 || step(cudaMemcpy(m->f, d->load.data, size_t(m->Qf) * N * sizeof(double),
+                                           cudaMemcpyHostToDevice), "upload f")) &&
+            step(cudaMalloc(&m->vel.S, size_t(m->vel.rows) * m->vel.kalloc * sizeof(double)), "cudaMalloc(S)");
   if (ok) {
-    build_velocity_operator<<<4 * m->num_sms, 256>>>(m->S, m->R, m->kalloc, dC, m->A, m->N, m->Ne, m->Q);
+    build_velocity_operator<<<4 * m->num_sms, 256>>>(m->vel.S, m->vel.rows, m->vel.kalloc, dC, Qc, dA, Qa, dhb, dhg,
+                                                     drho, m->N, m->Ne, Qb);
     ok = step(cudaGetLastError(), "build_velocity_operator") && step(cudaDeviceSynchronize(), "build S");
   }
-  cudaFree(dC);
-  if (!ok) return cleanup(g_last_error.find("memory") != std::string::npos ? RBNS_ERR_OUT_OF_MEMORY : RBNS_ERR_CUDA);
-  m->bytes = int64_t(m->R) * m->kalloc * 8 + Q * N * N * 8 + Q * N * 8;
-  int rc = make_tensor_map(&m->tmS, m->S, m->R, m->kalloc);
+  for (void* ptr : {static_cast<void*>(dC), static_cast<void*>(dA), static_cast<void*>(dhb),
+                    static_cast<void*>(dhg), static_cast<void*>(drho)})
+    if (ptr) cudaFree(ptr);
+  if (!ok) return bad();
+  m->bytes = m->vel.rows * m->vel.kalloc * 8 + int64_t(m->Qf) * N * 8 + int64_t(th.size()) * 24;
+  int rc = make_tensor_map(&m->vel.tm, m->vel.S, m->vel.rows, m->vel.kalloc);
   if (rc) return cleanup(rc);
 
   if (m->Np) {
@@ -509,22 +652,24 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
     else
       L.assign(size_t(np) * np, 0.0);
     double* dB = nullptr;
-    ok = step(cudaMalloc(&dB, size_t(Q) * np * N * sizeof(double)), "cudaMalloc(Bq)") &&
-         step(cudaMemcpy(dB, d->Bq, size_t(Q) * np * N * sizeof(double), cudaMemcpyHostToDevice), "upload Bq") &&
-         step(cudaMalloc(&m->Sp, size_t(np) * m->kalloc * sizeof(double)), "cudaMalloc(Sp)") &&
+    const int Qp = m->Qp;
+    ok = step(cudaMalloc(&dB, size_t(Qp) * np * N * sizeof(double)), "cudaMalloc(Bq)") &&
+         step(cudaMemcpy(dB, d->coupling.data, size_t(Qp) * np * N * sizeof(double), cudaMemcpyHostToDevice),
+              "upload Bq") &&
+         step(cudaMalloc(&m->prs.S, size_t(np) * m->prs.kalloc * sizeof(double)), "cudaMalloc(Sp)") &&
          step(cudaMalloc(&m->L, size_t(np) * np * sizeof(double)), "cudaMalloc(L)") &&
          step(cudaMalloc(&m->Lt, size_t(np) * np * sizeof(double)), "cudaMalloc(Lt)") &&
          step(cudaMemcpy(m->L, L.data(), size_t(np) * np * sizeof(double), cudaMemcpyHostToDevice), "upload L") &&
          step(cudaMemcpy(m->Lt, Lt.data(), size_t(np) * np * sizeof(double), cudaMemcpyHostToDevice), "upload Lt");
     if (ok) {
-      build_pressure_operator<<<m->num_sms, 256>>>(m->Sp, m->Np, m->kalloc, dB, m->N, m->Ne, m->Q);
+      build_pressure_operator<<<m->num_sms, 256>>>(m->prs.S, m->Np, m->prs.kalloc, dB, m->N, m->Ne, Qp);
       ok = step(cudaGetLastError(), "build_pressure_operator") && step(cudaDeviceSynchronize(), "build Sp");
     }
     if (dB) cudaFree(dB);
-    if (!ok) return cleanup(RBNS_ERR_CUDA);
-    rc = make_tensor_map(&m->tmSp, m->Sp, m->Np, m->kalloc);
+    if (!ok) return bad();
+    rc = make_tensor_map(&m->prs.tm, m->prs.S, m->Np, m->prs.kalloc);
     if (rc) return cleanup(rc);
-    m->bytes += np * m->kalloc * 8 + 2 * np * np * 8;
+    m->bytes += np * m->prs.kalloc * 8 + 2 * np * np * 8;
   }
   *out = m;
   return RBNS_OK;
@@ -533,7 +678,8 @@ int rbns_model_create(const rbns_model_desc* d, int device, rbns_model** out) {
 int rbns_model_destroy(rbns_model* m) {
   if (!m) return RBNS_OK;
   DeviceGuard guard(m->device);
-  for (double* p : {m->S, m->A, m->f, m->Sp, m->L, m->Lt})
+  for (void* p : {static_cast<void*>(m->vel.S), static_cast<void*>(m->prs.S), static_cast<void*>(m->f),
+                  static_cast<void*>(m->L), static_cast<void*>(m->Lt), static_cast<void*>(m->dth)})
     if (p) cudaFree(p);
   delete m;
   return RBNS_OK;
@@ -542,9 +688,20 @@ int rbns_model_destroy(rbns_model* m) {
 int rbns_model_info(const rbns_model* m, int32_t* n, int32_t* q, int32_t* n_p, int32_t* device) {
   if (!m) return fail(RBNS_ERR_INVALID_ARGUMENT, "model is NULL");
   if (n) *n = m->N;
-  if (q) *q = m->Q;
+  if (q) *q = m->Qc;
   if (n_p) *n_p = m->Np;
   if (device) *device = m->device;
+  return RBNS_OK;
+}
+
+int rbns_model_terms(const rbns_model* m, int32_t counts[6]) {
+  if (!m || !counts) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL argument");
+  counts[0] = m->Qa;
+  counts[1] = m->Qc;
+  counts[2] = m->Qf;
+  counts[3] = m->Qp;
+  counts[4] = m->vel.Qb;
+  counts[5] = m->G;
   return RBNS_OK;
 }
 
@@ -609,12 +766,15 @@ int rbns_reduced_operator(rbns_model* m, const double* mu, const double* eta, in
   if (B == 0) return RBNS_OK;
   DeviceGuard guard(m->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t ldy = m->row_tiles * kBN;
+  const int64_t ldy = m->vel.row_tiles * kBN;
   double* y = nullptr;
   RBNS_CUDA(cudaMallocAsync(&y, size_t(B) * ldy * sizeof(double), st));
-  int rc = launch_contract(m, m->tmS, m->row_tiles, nullptr, int(B), eta, mu, y, ldy, st);
+  int rc = launch_contract(m, m->vel, nullptr, int(B), eta, mu, y, ldy, st);
   if (rc == RBNS_OK) {
-    operator_readout<<<int(B), 128, 0, st>>>(y, ldy, int(B), eta, mu, m->f, m->N, m->Q, m->th, residual, jacobian);
+    NewtonParams np = newton_params(m);
+    np.n = int32_t(B);
+    np.mu = mu;
+    operator_readout<<<int(B), 128, 0, st>>>(y, ldy, eta, np, residual, jacobian);
     if (cudaGetLastError() != cudaSuccess) rc = fail(RBNS_ERR_CUDA, "operator_readout launch failed");
   }
   cudaFreeAsync(y, st);

@@ -3,13 +3,17 @@
 #pragma once
 
 #include "rbns_common.cuh"
+#include "rbns_newton.cuh"
 
 namespace rbns {
 
 // S[r][κ] for the contraction GEMM (layout documented in rbns_contract.cuh).  One-time, at model create.
+// hb/hg/rho: for each linear term a, the block and group of its h rows and its factor ρ_a
+// (θ_a = ρ_a · μ₁^{e_g} · θ_block, resolved on the host by rbns_model_create2).
 __global__ void build_velocity_operator(double* __restrict__ S, int64_t rows, int kalloc,
-                                        const double* __restrict__ C, const double* __restrict__ A, int N,
-                                        int Ne, int Q) {
+                                        const double* __restrict__ C, int Qc, const double* __restrict__ A, int Ql,
+                                        const int* __restrict__ hb, const int* __restrict__ hg,
+                                        const double* __restrict__ rho, int N, int Ne, int Qb) {
   const int64_t total = rows * kalloc;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
@@ -19,28 +23,31 @@ __global__ void build_velocity_operator(double* __restrict__ S, int64_t rows, in
     const int64_t nn = int64_t(N) * N;
     if (r < nn) {
       const int l = int(r / N), m = int(r - int64_t(l) * N);
-      if (kap < Q * Ne) {
+      if (kap < Qc * Ne) {
         const int q = kap / Ne, k = kap - q * Ne;
         if (k < N) {
           const int64_t base = int64_t(q) * N * nn;
           v = C[base + (int64_t(m) * N + k) * N + l] + C[base + (int64_t(k) * N + m) * N + l];
         }
-      } else if (kap < Q * Ne + Q) {
-        const int q = kap - Q * Ne;
-        v = A[(int64_t(q) * N + l) * N + m];
+      } else if (kap >= Qb * Ne && kap < Qb * Ne + Ql) {
+        const int a = kap - Qb * Ne;
+        v = A[(int64_t(a) * N + l) * N + m];
       }
-    } else if (r < nn + N) {
-      const int l = int(r - nn);
-      if (kap < Q * Ne) {
-        const int q = kap / Ne, k = kap - q * Ne;
-        if (k < N) v = A[(int64_t(q) * N + l) * N + k];
+    } else if (r < rows) {
+      const int g = int((r - nn) / N), l = int(r - nn - int64_t(g) * N);
+      if (kap < Qb * Ne) {
+        const int j = kap / Ne, k = kap - j * Ne;
+        if (k < N)
+          for (int a = 0; a < Ql; ++a)
+            if (hb[a] == j && hg[a] == g) v = fma(rho[a], A[(int64_t(a) * N + l) * N + k], v);
       }
     }
     S[idx] = v;
   }
 }
 
-// Sp[i][κ] = B_q[i][k] for κ = q·Ne + k: the recovery right-hand side Σ_q θ_q B_q u is the same GEMM.
+// Sp[i][κ] = B_q[i][k] for κ = q·Ne + k: the recovery right-hand side Σ_q θ_q B_q u is the same GEMM
+// (coupling family: Q blocks, no affine columns).
 __global__ void build_pressure_operator(double* __restrict__ S, int np, int kalloc, const double* __restrict__ Bq,
                                         int N, int Ne, int Q) {
   const int64_t total = int64_t(np) * kalloc;
@@ -161,28 +168,22 @@ __global__ void __launch_bounds__(256) pressure_trisolve(const double* __restric
   }
 }
 
-// reduced_operator readout: R = ½ J η + ½ ν A(μ)η − f(μ), J copied out (debug / FD path).
-__global__ void operator_readout(const double* __restrict__ Y, int64_t ldy, int32_t n, const double* __restrict__ eta,
-                                 const double* __restrict__ mu, const double* __restrict__ f, int N, int Q,
-                                 ThetaDesc th, double* __restrict__ R, double* __restrict__ Jout) {
+// reduced_operator readout: R = ½ J η + ½ L(μ)η − f(μ) (the Newton right-hand side, negated), J copied out
+// (debug / FD path).  p carries the load family and the h groups exactly as for the Newton kernel.
+__global__ void operator_readout(const double* __restrict__ Y, int64_t ldy, const double* __restrict__ eta,
+                                 const NewtonParams p, double* __restrict__ R, double* __restrict__ Jout) {
   const int b = blockIdx.x;
-  if (b >= n) return;
-  __shared__ double ths[RBNS_MAX_TERMS];
-  __shared__ double nus;
-  if (threadIdx.x == 0) {
-    const double alpha = mu[2 * b], re = mu[2 * b + 1];
-    nus = 1.0 / re;
-    for (int q = 0; q < Q; ++q) ths[q] = eval_theta_term(th, q, alpha, re);
-  }
+  if (b >= p.n) return;
+  __shared__ NewtonWeights w;
+  newton_weights(p, b, w);
   __syncthreads();
+  const int N = p.N;
   const double* Yb = Y + int64_t(b) * ldy;
   for (int64_t e = threadIdx.x; e < int64_t(N) * N; e += blockDim.x) Jout[int64_t(b) * N * N + e] = Yb[e];
   for (int l = threadIdx.x; l < N; l += blockDim.x) {
     double ju = 0.0;
     for (int m = 0; m < N; ++m) ju = fma(Yb[int64_t(l) * N + m], eta[int64_t(b) * N + m], ju);
-    double fl = 0.0;
-    for (int q = 0; q < Q; ++q) fl = fma(ths[q], f[q * N + l], fl);
-    R[int64_t(b) * N + l] = 0.5 * ju + 0.5 * nus * Yb[int64_t(N) * N + l] - fl;
+    R[int64_t(b) * N + l] = -newton_rhs(p, Yb, l, ju, w);
   }
 }
 

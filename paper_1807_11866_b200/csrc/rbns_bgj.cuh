@@ -37,8 +37,7 @@ struct BGJShared {
   static constexpr int NR = 8 * RT;
   static constexpr int PS = 9;                   // panel row stride (doubles): conflict-free column reads
   static constexpr int NB = 3;                   // panel buffers (P, P-1 pending, P+1 being factored)
-  double th[RBNS_MAX_TERMS];
-  double nu;
+  NewtonWeights w;
   int sing;
   int fail;                                      // speculative pass rejected: rerun with pivot search
   int nc[NB];                                    // columns factored in the panel of each buffer
@@ -396,10 +395,9 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
     for (int q = 0; q < NB; ++q) sh.rowpos[q][r] = -1;
   }
   __syncthreads();
-  const double nu = sh.nu;
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
 
-  // ---- load the owned tiles: J (or ν A(μ) at u = 0) ----
+  // ---- load the owned tiles of J ----
 #pragma unroll
   for (int jj = 0; jj < JJ; ++jj) {
     const int j = warp + NW * jj;
@@ -410,36 +408,25 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
       for (int e = 0; e < 2; ++e) {
         const int col = 8 * j + 2 * t + e;
         double v = 0.0;
-        if (j < CT && r < N && col < N) {
-          if (p.first) {
-            double s = 0.0;
-#pragma unroll 1
-            for (int q = 0; q < p.Q; ++q) s = fma(sh.th[q], __ldg(&p.A[(int64_t(q) * N + r) * N + col]), s);
-            v = nu * s;
-          } else {
-            v = __ldcs(&Jb[int64_t(r) * N + col]);
-          }
-        }
+        if (j < CT && r < N && col < N) v = __ldcs(&Jb[int64_t(r) * N + col]);
         acc[jj][i][e] = v;
       }
     }
   }
   if (warp == 0) RBNS_TR(spec ? 1 : 101);
 
-  // ---- right-hand side −R = f − ½ J u − ½ ν A(μ)u as column N ----
+  // ---- right-hand side −R = f − ½ J u − ½ L(μ)u as column N ----
   {
     double part[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) part[i] = 0.0;
-    if (!p.first) {
 #pragma unroll
-      for (int jj = 0; jj < JJ; ++jj) {
-        const int c0 = 8 * (warp + NW * jj) + 2 * t;
-        const double u0 = c0 < N ? p.u[int64_t(b) * N + c0] : 0.0;
-        const double u1 = c0 + 1 < N ? p.u[int64_t(b) * N + c0 + 1] : 0.0;
+    for (int jj = 0; jj < JJ; ++jj) {
+      const int c0 = 8 * (warp + NW * jj) + 2 * t;
+      const double u0 = c0 < N ? p.u[int64_t(b) * N + c0] : 0.0;
+      const double u1 = c0 + 1 < N ? p.u[int64_t(b) * N + c0 + 1] : 0.0;
 #pragma unroll
-        for (int i = 0; i < RT; ++i) part[i] = fma(acc[jj][i][0], u0, fma(acc[jj][i][1], u1, part[i]));
-      }
+      for (int i = 0; i < RT; ++i) part[i] = fma(acc[jj][i][0], u0, fma(acc[jj][i][1], u1, part[i]));
     }
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
@@ -454,11 +441,7 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
         double ju = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) ju += sh.rowred[w][r];
-        double fi = 0.0;
-#pragma unroll 4
-        for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + r]), fi);
-        const double h = p.first ? 0.0 : Jb[int64_t(N) * N + r];
-        rhs = fi - 0.5 * ju - 0.5 * nu * h;
+        rhs = newton_rhs(p, Jb, r, ju, sh.w);
       }
       sh.rhs[r] = rhs;
     }
@@ -540,11 +523,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int N = p.N;
 
-  if (tid == 0) {
-    const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
-    sh.nu = 1.0 / re;
-    for (int q = 0; q < p.Q; ++q) sh.th[q] = eval_theta_term(p.th, q, alpha, re);
-  }
+  newton_weights(p, b, sh.w);
   __syncthreads();
   double acc[JJ][RT][2];
   if (warp == 0) RBNS_TR(0);
@@ -576,7 +555,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   if (!sing) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.pivval[k];
-      const double unew = (p.first ? 0.0 : p.u[int64_t(b) * N + k]) + x;
+      const double unew = p.u[int64_t(b) * N + k] + x;
       d2 = fma(x, x, d2);
       un2 = fma(unew, unew, un2);
     }
@@ -587,8 +566,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   if (!sing && finite) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.pivval[k];
-      const double uold = p.first ? 0.0 : p.u[int64_t(b) * N + k];
-      p.u[int64_t(b) * N + k] = uold + x;
+      p.u[int64_t(b) * N + k] += x;
     }
   }
   if (tid == 0) {

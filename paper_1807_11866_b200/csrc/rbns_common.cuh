@@ -22,33 +22,29 @@ __device__ unsigned long long g_trace[256];
 
 constexpr int kStatusActive = 127;  // internal: sample still iterating
 
-struct ThetaDesc {
-  int32_t q;
-  int32_t kind[RBNS_MAX_TERMS];
-  int32_t k[RBNS_MAX_TERMS];
-  int32_t m[RBNS_MAX_TERMS];
-  double scale[RBNS_MAX_TERMS];
-};
-
 __device__ __forceinline__ double ipow(double x, int n) {
   double r = 1.0;
   for (int i = 0; i < n; ++i) r = r * x;
   return r;
 }
 
-// θ_q(μ) — same rule, term by term, as paper_1807_11866_b200/affine.py:evaluate_weights
-// (SPEC.md:360-368 evaluate_weights; SPEC.md:335-338 CoefficientDescriptor).
-__device__ __forceinline__ double eval_theta_term(const ThetaDesc& d, int q, double alpha, double re) {
+// θ(μ) of one descriptor (the C-ABI rbns_theta_term, copied to device memory at model create) — same rule,
+// term by term, as paper_1807_11866_b200/affine.py:evaluate_weights (SPEC.md:360-368 evaluate_weights;
+// SPEC.md:335-338 CoefficientDescriptor "scale·φᵏ·u∞ᵐ").  μ = (mu0, mu1) = (α or φ, Re or u∞).
+__device__ __forceinline__ double eval_theta(const rbns_theta_term& t, double mu0, double mu1) {
   double base;
-  switch (d.kind[q]) {
+  switch (t.kind) {
     case RBNS_THETA_CONST: base = 1.0; break;
-    case RBNS_THETA_COS_K: base = cos(double(d.k[q]) * alpha); break;
-    case RBNS_THETA_SIN_K: base = sin(double(d.k[q]) * alpha); break;
-    case RBNS_THETA_COS_SIN_POW: base = ipow(cos(alpha), d.k[q]) * ipow(sin(alpha), d.m[q]); break;
-    default: base = ipow(alpha, d.k[q]) * ipow(re, d.m[q]); break;
+    case RBNS_THETA_COS_K: base = cos(double(t.k) * mu0); break;
+    case RBNS_THETA_SIN_K: base = sin(double(t.k) * mu0); break;
+    case RBNS_THETA_COS_SIN_POW: base = ipow(cos(mu0), t.k) * ipow(sin(mu0), t.m); break;
+    default: base = ipow(mu0, t.k) * ipow(mu1, t.m); break;
   }
-  return d.scale[q] * base;
+  return t.scale * base;
 }
+
+// μ₁^e for the residual's h-group factors (e = −1: ν = 1/Re)
+__device__ __forceinline__ double mu1_pow(double mu1, int e) { return e >= 0 ? ipow(mu1, e) : 1.0 / ipow(mu1, -e); }
 
 // ---------------------------------------------------------------------------------------------------------
 // PTX wrappers

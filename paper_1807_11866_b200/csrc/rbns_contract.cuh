@@ -2,11 +2,14 @@
 // FP64 tensor-core (DMMA) GEMM over the μ batch.
 //
 //   Y[b][r] = Σ_κ X[b][κ] · S[r][κ]
-//     rows r < N²       : r = l·N + m  -> Jacobian entry J[l][m] = ν A(μ)[l][m] + Σ_q θ_q Σ_k S_q[m,k,l] u_k
-//     rows N² ≤ r < N²+N: r = N² + l   -> h[l] = (A(μ) u)[l]                   (residual helper)
-//     cols κ = q·Ne + k  : X = θ_q(μ_b) · u_b[k]           S = S_q[m,k,l] = C_q[m,k,l] + C_q[k,m,l]
-//     cols κ = Q·Ne + q  : X = ν_b · θ_q(μ_b)              S = A_q[l][m]
-// (PAPER.md:797-805 affine sums; PAPER.md:821-844 tensor + Fréchet chain.)
+//     rows r < N²        : r = l·N + m    -> J[l][m] = L(μ)[l][m] + Σ_c θ_c Σ_k S_c[m,k,l] u_k
+//     rows N² + g·N + l  : group g of G   -> h_g[l], with L(μ)u = Σ_g μ₁^{e_g} h_g   (residual helper)
+//     cols κ = j·Ne + k  : block j < Qb   X = θ_j(μ_b) · u_b[k]     S = S_j[m,k,l] = C_j[m,k,l] + C_j[k,m,l]
+//                                                                   (h rows: ρ_a A_a[l][k] of the linear terms
+//                                                                    tied to block j; extra blocks: h only)
+//     cols κ = Qb·Ne + a : linear term a  X = [ν_b] θ_a(μ_b)       S = A_a[l][m]
+// (PAPER.md:797-805 affine sums; PAPER.md:821-844 tensor + Fréchet chain.)  The BASELINE
+// configs have one θ list for every family: Qb = Qa = Q, G = 1, e = −1 (h = A(μ)u times ν).
 //
 // Dataflow (one CTA = BM samples × a range of BN-row tiles):
 //   * S (the μ-independent operand, 56 MB at N=100/Q=7) is streamed from L2 by TMA (cp.async.bulk.tensor,
@@ -31,17 +34,20 @@ struct ContractParams {
   int32_t n;              // samples in this chunk
   const double* u;        // [B][N] states, indexed by sample id
   const double* mu;       // [B][2]
-  int32_t N, Ne, Q;       // Ne = κ stride per term (N rounded up to a multiple of 4)
+  int32_t N, Ne;          // Ne = κ stride per block (N rounded up to a multiple of 4)
+  int32_t Qb, Ql;         // contraction blocks (θ ⊗ u) and affine columns
+  int32_t nu_lin;         // affine columns carry ν = 1/μ₁
+  const rbns_theta_term* thb;  // [Qb] block descriptors (device)
+  const rbns_theta_term* thl;  // [Ql] affine-column descriptors (device)
   int32_t nchunks;        // TMA stages per row tile (8 κ each)
   int32_t nsub;           // k4 sub-steps per row tile (= K / 4)
-  int32_t sub_begin;      // first k4 sub-step (Q·Ne/4 at u = 0: only the ν θ_q A_q block is non-zero)
+  int32_t sub_begin;      // first k4 sub-step (Qb·Ne/4 at u = 0: only the affine block is non-zero)
   int32_t row_tiles;      // ceil(R / BN)
   int32_t tiles_per_group;
   int32_t ldu_s;          // shared-memory row stride of the u tile (≡ 8 mod 16)
   int32_t stages;
   double* out;            // [n][ldo]
   int64_t ldo;
-  ThetaDesc th;
 };
 
 #ifndef RBNS_BN
@@ -59,9 +65,9 @@ constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 // u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups
 __host__ __device__ inline int contract_ldu(int ne) { return ne + ((4 - ne % 16) + 16) % 16; }
 
-__host__ inline size_t contract_smem_bytes(int stages, int ldu, int q) {
+__host__ inline size_t contract_smem_bytes(int stages, int ldu, int qb, int ql) {
   return size_t(stages) * 2 * kBN * 4 * sizeof(double) + size_t(kBM) * ldu * sizeof(double) +
-         2 * size_t(q) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
+         size_t(qb + ql) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
 }
 
 #ifdef RBNS_CONTRACT_MAXNREG
@@ -82,8 +88,8 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
   double* Sst = reinterpret_cast<double*>(smem_raw);
   double* Us = Sst + size_t(p.stages) * STAGE;
   double* thS = Us + size_t(BM) * p.ldu_s;
-  double* thnuS = thS + p.Q * BM;
-  uint64_t* full = reinterpret_cast<uint64_t*>(thnuS + p.Q * BM);
+  double* thnuS = thS + p.Qb * BM;
+  uint64_t* full = reinterpret_cast<uint64_t*>(thnuS + p.Ql * BM);
   uint64_t* empty = full + p.stages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -101,7 +107,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
   }
   if (warp == NCW && lane == 0) prefetch_tmap(&tmap);
 
-  // resident u tile (zero-padded in k and beyond the chunk) and θ, νθ for the tile's samples
+  // resident u tile (zero-padded in k and beyond the chunk) and the block / affine weights of the tile's samples
   for (int idx = threadIdx.x; idx < BM * p.ldu_s; idx += blockDim.x) {
     const int b = idx / p.ldu_s, k = idx - b * p.ldu_s;
     const int i = tile0 + b;
@@ -113,15 +119,13 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
     const int i = tile0 + b;
     if (i < p.n) {
       const int id = p.act ? p.act[i] : i;
-      const double alpha = p.mu[2 * id], re = p.mu[2 * id + 1];
-      const double nu = 1.0 / re;
-      for (int q = 0; q < p.Q; ++q) {
-        const double th = eval_theta_term(p.th, q, alpha, re);
-        thS[q * BM + b] = th;
-        thnuS[q * BM + b] = nu * th;
-      }
+      const double mu0 = p.mu[2 * id], mu1 = p.mu[2 * id + 1];
+      const double nu = p.nu_lin ? 1.0 / mu1 : 1.0;
+      for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = eval_theta(p.thb[q], mu0, mu1);
+      for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = nu * eval_theta(p.thl[q], mu0, mu1);
     } else {
-      for (int q = 0; q < p.Q; ++q) thS[q * BM + b] = thnuS[q * BM + b] = 0.0;
+      for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = 0.0;
+      for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = 0.0;
     }
   }
   __syncthreads();
@@ -153,7 +157,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
   const int wm = warp / WN, wn = warp % WN;
   const int g = lane >> 2, t = lane & 3;
   const int sb0 = wm * TM, rb0 = wn * TN;
-  const int kterms = p.Q * p.Ne;  // κ where the ν θ_q (linear) block starts
+  const int kterms = p.Qb * p.Ne;  // κ where the affine (linear) columns start
   int stage = 0;
   uint32_t phase = 0;
 
@@ -185,7 +189,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
           if (k0 == p.Ne) {
             k0 = 0;
             ++q;
-            if (q < p.Q) {
+            if (q < p.Qb) {
 #pragma unroll
               for (int mi = 0; mi < MI; ++mi) thq[mi] = thS[q * BM + sb0 + mi * 8 + g];
             }
@@ -193,7 +197,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
         } else {
           const int lin = kap - kterms + t;
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Q ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
+          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Ql ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
         }
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) bf[ni] = st[(j * BN + rb0 + ni * 8 + g) * 4 + t];
@@ -232,7 +236,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
         } else {
           const int lin = kap - kterms + t;
 #pragma unroll
-          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Q ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
+          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Ql ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
         }
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) bf[ni] = st[(j * BN + rb0 + ni * 8 + g) * 4 + t];

@@ -12,10 +12,9 @@
 // 91 register doubles per thread, two CTAs per SM); N ≤ 127 runs eight warps (16×16).
 //
 // Reference: dense LU with partial pivoting; Newton step and stop rule (SPEC.md:520-523,
-// SPEC.md:557-559); residual R = ν A(μ)u + Σθ_q C_q(u,u) − f(μ) evaluated as ½ J u + ½ ν A(μ)u − f(μ)
-// (Euler identity for the quadratic term; J and A(μ)u come from the contraction GEMM).  At u = 0 (first
-// Newton step) the convective part vanishes identically, so J = ν A(μ) is assembled here from the affine
-// terms ("η = 0 → Jacobian = linear blocks only") and the GEMM is skipped.
+// SPEC.md:557-559); residual R = L(μ)u + Σθ_c C_c(u,u) − f(μ) evaluated as ½ J u + ½ L(μ)u − f(μ)
+// (Euler identity for the quadratic term; J and the L(μ)u groups come from the contraction GEMM, which at
+// u = 0 runs only its affine block: "η = 0 → Jacobian = linear blocks only").
 #pragma once
 
 #include "rbns_common.cuh"
@@ -23,30 +22,54 @@
 namespace rbns {
 
 struct NewtonParams {
-  const int32_t* act;   // sample ids of this chunk
+  const int32_t* act;          // sample ids of this chunk
   int32_t n;
-  const double* J;      // [n][ldj]: rows 0..N²-1 Jacobian (row-major l,m), N²..N²+N-1 h = A(μ)u
+  const double* J;             // [n][ldj]: rows 0..N²-1 Jacobian (row-major l,m), then G groups of N rows h_g
   int64_t ldj;
-  double* u;            // [B][N] in/out
-  const double* mu;     // [B][2]
-  const double* A;      // [Q][N][N]
-  const double* f;      // [Q][N]
-  int32_t N, Q;
-  int32_t first;        // 1: u == 0, assemble J = ν A(μ) from A_q
+  double* u;                   // [B][N] in/out
+  const double* mu;            // [B][2]
+  const double* f;             // [Qf][N] load terms
+  const rbns_theta_term* thf;  // [Qf] their descriptors (device)
+  int32_t N, Qf;
+  int32_t G;                   // L(μ)u = Σ_g μ₁^{ge[g]} h_g   (G = 1, ge = −1: ν A(μ)u of the BASELINE configs)
+  int32_t ge[RBNS_MAX_GROUPS];
   int32_t iter, max_iter;
   double tol;
   int32_t* iters;
   int8_t* status;
   double* last;
-  ThetaDesc th;
 };
+
+// Per-sample residual weights, evaluated once per CTA into shared memory.
+struct NewtonWeights {
+  double th[RBNS_MAX_TERMS];  // θ_f(μ) of the load terms
+  double gf[RBNS_MAX_GROUPS]; // μ₁^{ge[g]}
+};
+
+__device__ __forceinline__ void newton_weights(const NewtonParams& p, int b, NewtonWeights& w) {
+  const double mu0 = p.mu[2 * b], mu1 = p.mu[2 * b + 1];
+  for (int q = threadIdx.x; q < p.Qf; q += blockDim.x) w.th[q] = eval_theta(p.thf[q], mu0, mu1);
+  if (threadIdx.x < p.G) w.gf[threadIdx.x] = mu1_pow(mu1, p.ge[threadIdx.x]);
+}
+
+// Newton right-hand side entry i: −R_i = f(μ)_i − ½ (J u)_i − ½ (L(μ) u)_i  (Euler identity J_c u = 2 C(u,u);
+// J and the h groups come from the contraction kernel).  ju = (J u)_i.
+__device__ __forceinline__ double newton_rhs(const NewtonParams& p, const double* Jb, int i, double ju,
+                                             const NewtonWeights& w) {
+  const int N = p.N;
+  double fi = 0.0;
+#pragma unroll 4
+  for (int q = 0; q < p.Qf; ++q) fi = fma(w.th[q], __ldg(&p.f[q * N + i]), fi);
+  double h = 0.0;
+  for (int g = 0; g < p.G; ++g) h = fma(w.gf[g], Jb[int64_t(N) * N + int64_t(g) * N + i], h);
+  return fi - 0.5 * ju - 0.5 * h;
+}
 
 template <int TGR, int TGC, int RS, int CS>
 struct GJShared {
   static constexpr int NW = (TGR * TGC + 31) / 32;
   static constexpr int CBS = RS | 1;  // odd stride: conflict-free column reads by 8 thread-rows
-  double th[RBNS_MAX_TERMS];
-  double nu;
+  NewtonWeights w;
   double pv;                          // current pivot value (signed), from the owner warp
   int pk;                             // current pivot row (-1: singular)
   double colbuf[2][TGR][CBS];         // pivot column, thread-row major
@@ -187,41 +210,20 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
 
-  if (tid == 0) {
-    const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
-    sh.nu = 1.0 / re;
-    for (int q = 0; q < p.Q; ++q) sh.th[q] = eval_theta_term(p.th, q, alpha, re);
-  }
+  newton_weights(p, b, sh.w);
   __syncthreads();
-  const double nu = sh.nu;
 
   double a[RS][CS];
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
-  if (p.first) {
 #pragma unroll
-    for (int r = 0; r < RS; ++r)
+  for (int r = 0; r < RS; ++r)
 #pragma unroll
-      for (int s = 0; s < CS; ++s) {
-        const int i = tr + TGR * r, j = tc + TGC * s;
-        double v = 0.0;
-        if (i < N && j < N) {
-          double acc = 0.0;
-          for (int q = 0; q < p.Q; ++q) acc = fma(sh.th[q], __ldg(&p.A[(int64_t(q) * N + i) * N + j]), acc);
-          v = nu * acc;
-        }
-        a[r][s] = v;
-      }
-  } else {
-#pragma unroll
-    for (int r = 0; r < RS; ++r)
-#pragma unroll
-      for (int s = 0; s < CS; ++s) {
-        const int i = tr + TGR * r, j = tc + TGC * s;
-        a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
-      }
-  }
+    for (int s = 0; s < CS; ++s) {
+      const int i = tr + TGR * r, j = tc + TGC * s;
+      a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
+    }
 
-  // right-hand side −R = f − ½ J u − ½ ν A(μ)u, stored as column N.  J u: per-thread partial row sums,
+  // right-hand side −R = f − ½ J u − ½ L(μ)u, stored as column N.  J u: per-thread partial row sums,
   // lane shuffles across the thread-columns inside a warp, then a fixed-order sum over warps.
   {
     constexpr int NW = GJShared<TGR, TGC, RS, CS>::NW;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
 #pragma unroll
     for (int s = 0; s < CS; ++s) {
       const int j = tc + TGC * s;
-      uj[s] = (!p.first && j < N) ? p.u[int64_t(b) * N + j] : 0.0;
+      uj[s] = j < N ? p.u[int64_t(b) * N + j] : 0.0;
     }
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -248,10 +250,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
         double ju = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) ju += sh.rowred[w][i];
-        double fi = 0.0;
-        for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
-        const double h = p.first ? 0.0 : Jb[int64_t(N) * N + i];
-        rhs = fi - 0.5 * ju - 0.5 * nu * h;
+        rhs = newton_rhs(p, Jb, i, ju, sh.w);
       }
       sh.rhs[i] = rhs;
     }
@@ -283,7 +282,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
   if (!sing) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
-      const double unew = (p.first ? 0.0 : p.u[int64_t(b) * N + k]) + x;
+      const double unew = p.u[int64_t(b) * N + k] + x;
       d2 = fma(x, x, d2);
       un2 = fma(unew, unew, un2);
     }
@@ -294,8 +293,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
   if (!sing && finite) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
-      const double uold = p.first ? 0.0 : p.u[int64_t(b) * N + k];
-      p.u[int64_t(b) * N + k] = uold + x;
+      p.u[int64_t(b) * N + k] += x;
     }
   }
   if (tid == 0) {

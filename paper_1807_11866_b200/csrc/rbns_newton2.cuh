@@ -28,8 +28,7 @@ struct GJ2Shared {
   static constexpr int NT = TGR * TGC;
   static constexpr int NW = (NT + 31) / 32;
   static constexpr int NR = TGR * RS;
-  double th[RBNS_MAX_TERMS];
-  double nu;
+  NewtonWeights w;
   double col[2][NR];             // pivot column (row-indexed), double-buffered by step parity
   struct alignas(16) Cand {
     unsigned long long key;      // |a| bits (sign cleared): orders like |a|
@@ -164,7 +163,7 @@ __device__ __forceinline__ void gj2_block(double (&a)[RS][CS], bool& sing, const
 }
 
 // Kernel prologue shared by the register Gauss–Jordan variants: θ(μ), ν, the J tile into registers and the
-// right-hand side −R = f − ½ J u − ½ ν A(μ)u as column N.  SH needs th, nu, pivoted, rowred, rhs.
+// right-hand side −R = f − ½ J u − ½ L(μ)u as column N.  SH needs w, pivoted, rowred, rhs.
 template <int TGR, int TGC, int RS, int CS, class SH>
 __device__ __forceinline__ void gj_load_system(const NewtonParams& p, int i_s, int b, double (&a)[RS][CS], SH& sh) {
   constexpr int NT = TGR * TGC;
@@ -172,14 +171,9 @@ __device__ __forceinline__ void gj_load_system(const NewtonParams& p, int i_s, i
   constexpr int NR = TGR * RS;
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
-  if (tid == 0) {
-    const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
-    sh.nu = 1.0 / re;
-    for (int q = 0; q < p.Q; ++q) sh.th[q] = eval_theta_term(p.th, q, alpha, re);
-  }
+  newton_weights(p, b, sh.w);
   for (int r = tid; r < NR; r += NT) sh.pivoted[r] = 0;
   __syncthreads();
-  const double nu = sh.nu;
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
 #pragma unroll
   for (int r = 0; r < RS; ++r)
@@ -211,10 +205,7 @@ __device__ __forceinline__ void gj_load_system(const NewtonParams& p, int i_s, i
       double ju = 0.0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) ju += sh.rowred[w][i];
-      double fi = 0.0;
-#pragma unroll 4
-      for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
-      rhs = fi - 0.5 * ju - 0.5 * nu * Jb[int64_t(N) * N + i];
+      rhs = newton_rhs(p, Jb, i, ju, sh.w);
     }
     sh.rhs[i] = rhs;
   }

@@ -21,8 +21,7 @@ template <int TGR, int TGC, int RS, int CS>
 struct GJCShared {
   static constexpr int NW = TGR * TGC / 32;
   static constexpr int CBS = RS | 1;
-  double th[RBNS_MAX_TERMS];
-  double nu;
+  NewtonWeights w;
   double pv[2];
   int pk[2];
   double colbuf[2][TGR][CBS];
@@ -142,18 +141,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
   const int rhs_rank = (N % (2 * TGC)) / TGC, rhs_tc = N % TGC, rhs_slot = N / (2 * TGC);
   auto gcol = [&](int s) { return s * 2 * TGC + rank * TGC + tc; };
 
-  if (tid == 0 && live) {
-    const double alpha = p.mu[2 * b], re = p.mu[2 * b + 1];
-    sh.nu = 1.0 / re;
-    for (int q = 0; q < p.Q; ++q) sh.th[q] = eval_theta_term(p.th, q, alpha, re);
-  }
+  if (live) newton_weights(p, b, sh.w);
   __syncthreads();
   if (!live) {
     cluster.sync();
     return;
   }
-  const double nu = sh.nu;
-
   double a[RS][CS];
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
 #pragma unroll
@@ -161,27 +154,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
 #pragma unroll
     for (int s = 0; s < CS; ++s) {
       const int i = tr + TGR * r, j = gcol(s);
-      double v = 0.0;
-      if (i < N && j < N) {
-        if (p.first) {
-          double acc = 0.0;
-#pragma unroll 1
-          for (int q = 0; q < p.Q; ++q) acc = fma(sh.th[q], __ldg(&p.A[(int64_t(q) * N + i) * N + j]), acc);
-          v = nu * acc;
-        } else {
-          v = __ldcs(&Jb[int64_t(i) * N + j]);
-        }
-      }
-      a[r][s] = v;
+      a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
     }
 
-  // right-hand side −R = f − ½ J u − ½ ν A(μ)u as column N (owned by CTA rhs_rank)
+  // right-hand side −R = f − ½ J u − ½ L(μ)u as column N (owned by CTA rhs_rank)
   {
     double uj[CS];
 #pragma unroll
     for (int s = 0; s < CS; ++s) {
       const int j = gcol(s);
-      uj[s] = (!p.first && j < N) ? p.u[int64_t(b) * N + j] : 0.0;
+      uj[s] = j < N ? p.u[int64_t(b) * N + j] : 0.0;
     }
     const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
@@ -207,11 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
         double rhs = 0.0;
         if (i < N) {
           const double ju = sh.xred[0][i] + sh.xred[1][i];
-          double fi = 0.0;
-#pragma unroll 1
-          for (int q = 0; q < p.Q; ++q) fi = fma(sh.th[q], __ldg(&p.f[q * N + i]), fi);
-          const double h = p.first ? 0.0 : Jb[int64_t(N) * N + i];
-          rhs = fi - 0.5 * ju - 0.5 * nu * h;
+          rhs = newton_rhs(p, Jb, i, ju, sh.w);
         }
         sh.rhs[i] = rhs;
       }
@@ -243,7 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
     if (!sing) {
       for (int k = tid; k < N; k += NT) {
         const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
-        const double unew = (p.first ? 0.0 : p.u[int64_t(b) * N + k]) + x;
+        const double unew = p.u[int64_t(b) * N + k] + x;
         d2 = fma(x, x, d2);
         un2 = fma(unew, unew, un2);
       }
@@ -254,8 +232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
     if (!sing && finite) {
       for (int k = tid; k < N; k += NT) {
         const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
-        const double uold = p.first ? 0.0 : p.u[int64_t(b) * N + k];
-        p.u[int64_t(b) * N + k] = uold + x;
+        p.u[int64_t(b) * N + k] += x;
       }
     }
     if (tid == 0) {

@@ -1,12 +1,24 @@
 """``ReducedModel`` — the hot path's input contract.
 
-Only the fields the velocity-only block solver consumes are carried: per affine term q the projected viscous
-matrix A_q (N×N), the convective tensor C_q (N×N×N, C[j,k,l] = c(u_j advecting, u_k advected, u_l test);
-PAPER.md:821-827, index convention cross-checked against the reference assembler
-``assemble.convection_matrices`` /root/reference/pkg/src/rbflow/assemble.py:86-101 by tests/golden), the load
-vector f_q (N) and the θ descriptors.  Optional pressure-recovery operators (BASELINE.json config 4,
-SURVEY.md Appendix B #7): an SPD, μ-independent pressure Gramian M_p (Np×Np, the role of B_sp,
-PAPER.md:905-908) and coupling operators B_q (Np×N), recovering p = M_p⁻¹ Σ_q θ_q(μ) B_q u.
+Only the fields the velocity-only block solver consumes are carried, grouped in the SPEC's per-form term
+families (``AffineFormSet``) as they enter the reduced residual:
+
+    R(u) = L(μ) u + Σ_c θ_c(μ) C_c(u, u) − Σ_f θ_f(μ) f_f,         L(μ) = [ν] Σ_a θ_a(μ) A_a
+
+* ``A``  (Qa, N, N)    linear family: the viscous a-terms and, for lifted models, the lift-convection
+                        c0-terms (everything linear in u);
+* ``C``  (Qc, N, N, N) quadratic family: convective tensors C[j,k,l] = c(u_j advecting, u_k advected, u_l test)
+                        (index convention pinned against the reference assembler
+                        ``assemble.convection_matrices``, /root/reference/pkg/src/rbflow/assemble.py:86-101, by
+                        tests/golden);
+* ``f``  (Qf, N)       load family: projected loads and the lift's d0 terms (u∞¹ and u∞² families);
+* ``Bq`` (Qb, Np, N) + SPD ``Mp`` (Np, Np): optional pressure recovery M_p p = Σ_b θ_b(μ) B_b u
+                        (BASELINE.json config 4; the role of B_sp).
+
+Descriptors: ``theta`` is the shared list of the BASELINE configs (one θ per term index for every family);
+the ``theta_*`` fields override it per family (the paper's models: a-terms ν·φᵏ, c-terms φᵏ, c0-terms u∞·φᵏ,
+d0-terms u∞·φᵏ and u∞²·φᵏ).  ``nu_linear`` multiplies the linear family by ν = 1/μ₁ (the
+BASELINE rule); the paper's a-term descriptors carry ν in their scale instead (nu_linear=False).
 
 Immutable after construction and safe to share across concurrent queries.
 """
@@ -14,63 +26,98 @@ Immutable after construction and safe to share across concurrent queries (SPEC.m
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
 from .affine import MAX_TERMS, ThetaTerm
 
+FAMILIES = ("linear", "quadratic", "load", "coupling")
+
 
 @dataclass(frozen=True)
 class ReducedModel:
-    A: np.ndarray                      # (Q, N, N)   projected a-terms (multiplied by ν online)
-    C: np.ndarray                      # (Q, N, N, N) convective tensors
-    f: np.ndarray                      # (Q, N)      projected loads
-    theta: Sequence[ThetaTerm]         # Q descriptors
-    Mp: Optional[np.ndarray] = None    # (Np, Np)    SPD pressure Gramian (B_sp)
-    Bq: Optional[np.ndarray] = None    # (Q, Np, N)  pressure coupling terms (A_sv role)
+    A: np.ndarray                      # (Qa, N, N)     linear family
+    C: np.ndarray                      # (Qc, N, N, N)  quadratic family
+    f: np.ndarray                      # (Qf, N)        load family
+    theta: Sequence[ThetaTerm] = ()    # shared descriptors (every family), BASELINE configs
+    Mp: Optional[np.ndarray] = None    # (Np, Np)       SPD pressure Gramian (B_sp)
+    Bq: Optional[np.ndarray] = None    # (Qb, Np, N)    pressure coupling terms (A_sv role)
     name: str = "reduced-model"
     meta: dict = field(default_factory=dict, compare=False)
+    theta_linear: Optional[Sequence[ThetaTerm]] = None
+    theta_quadratic: Optional[Sequence[ThetaTerm]] = None
+    theta_load: Optional[Sequence[ThetaTerm]] = None
+    theta_coupling: Optional[Sequence[ThetaTerm]] = None
+    nu_linear: bool = True
 
     def __post_init__(self):
         A = np.ascontiguousarray(self.A, dtype=np.float64)
         C = np.ascontiguousarray(self.C, dtype=np.float64)
         f = np.ascontiguousarray(self.f, dtype=np.float64)
-        object.__setattr__(self, "A", A)
-        object.__setattr__(self, "C", C)
-        object.__setattr__(self, "f", f)
+        for name, arr in (("A", A), ("C", C), ("f", f)):
+            object.__setattr__(self, name, arr)
         object.__setattr__(self, "theta", tuple(self.theta))
-        q, n = f.shape
-        if A.shape != (q, n, n) or C.shape != (q, n, n, n):
+        if f.ndim != 2 or A.ndim != 3 or C.ndim != 4:
+            raise ValueError(f"operator ranks: A{A.shape} C{C.shape} f{f.shape}")
+        n = A.shape[1]
+        if A.shape[1:] != (n, n) or C.shape[1:] != (n, n, n) or f.shape[1] != n:
             raise ValueError(f"inconsistent operator shapes A{A.shape} C{C.shape} f{f.shape}")
-        if len(self.theta) != q:
-            raise ValueError(f"{len(self.theta)} theta descriptors for {q} affine terms")
-        if not 1 <= q <= MAX_TERMS:
-            raise ValueError(f"Q={q} outside [1, {MAX_TERMS}]")
         if (self.Mp is None) != (self.Bq is None):
             raise ValueError("pressure recovery needs both Mp and Bq")
         if self.Mp is not None:
             Mp = np.ascontiguousarray(self.Mp, dtype=np.float64)
             Bq = np.ascontiguousarray(self.Bq, dtype=np.float64)
             npr = Mp.shape[0]
-            if Mp.shape != (npr, npr) or Bq.shape != (q, npr, n):
+            if Mp.shape != (npr, npr) or Bq.ndim != 3 or Bq.shape[1:] != (npr, n) or npr < 1:
                 raise ValueError(f"inconsistent pressure shapes Mp{Mp.shape} Bq{Bq.shape}")
             object.__setattr__(self, "Mp", Mp)
             object.__setattr__(self, "Bq", Bq)
+        counts = {"linear": A.shape[0], "quadratic": C.shape[0], "load": f.shape[0],
+                  "coupling": 0 if self.Bq is None else self.Bq.shape[0]}
+        for fam in FAMILIES:
+            own = getattr(self, f"theta_{fam}")
+            terms = tuple(own) if own is not None else self.theta
+            if own is None and fam == "coupling" and self.Bq is None:
+                terms = ()
+            if len(terms) != counts[fam]:
+                raise ValueError(f"{len(terms)} theta descriptors for {counts[fam]} {fam} terms")
+            if counts[fam] > MAX_TERMS:
+                raise ValueError(f"{counts[fam]} {fam} terms > {MAX_TERMS}")
+            object.__setattr__(self, f"theta_{fam}", terms)
+        if counts["linear"] < 1:
+            raise ValueError("the linear family needs at least one term")
+        if self.Bq is not None and counts["coupling"] < 1:
+            raise ValueError("pressure recovery needs at least one coupling term")
+        object.__setattr__(self, "nu_linear", bool(self.nu_linear))
         for arr in (A, C, f):
             arr.flags.writeable = False
 
     @property
     def n(self) -> int:
-        return self.f.shape[1]
+        return self.A.shape[1]
 
     @property
     def q(self) -> int:
-        return self.f.shape[0]
+        """Number of quadratic (convective) terms — the Q of BASELINE.json's configs."""
+        return self.C.shape[0]
 
     @property
     def n_p(self) -> int:
         return 0 if self.Mp is None else self.Mp.shape[0]
+
+    @property
+    def counts(self) -> Tuple[int, int, int, int]:
+        """(linear, quadratic, load, coupling) term counts."""
+        return (self.A.shape[0], self.C.shape[0], self.f.shape[0], 0 if self.Bq is None else self.Bq.shape[0])
+
+    @property
+    def shared_theta(self) -> bool:
+        """True when every family uses one descriptor list (the BASELINE configs)."""
+        fams = [self.theta_linear, self.theta_quadratic, self.theta_load]
+        if self.Bq is not None:
+            fams.append(self.theta_coupling)
+        return all(t == fams[0] for t in fams)
 
     @property
     def theta_list(self) -> List[ThetaTerm]:

@@ -73,8 +73,29 @@ class BatchSolution:
     stats: Dict[str, float] = field(default_factory=dict)
 
 
+def _native_desc(model: ReducedModel):
+    """rbns_model_desc2 for a model (per-family descriptors, include/rbns.h); returns (desc, keep-alive list)."""
+    desc = _native.ModelDesc2C()
+    desc.n, desc.n_p = model.n, model.n_p
+    desc.flags = _native.NU_LINEAR if model.nu_linear else 0
+    keep = []
+    fams = (("linear", model.A), ("quadratic", model.C), ("load", model.f), ("coupling", model.Bq))
+    for name, data in fams:
+        terms = getattr(model, f"theta_{name}")
+        arr = (_native.ThetaTermC * max(1, len(terms)))()
+        for i, t in enumerate(terms):
+            arr[i] = _native.ThetaTermC(t.kind, t.k, t.m, 0, t.scale)
+        keep.append(arr)
+        fam = getattr(desc, name)
+        fam.count = len(terms) if data is not None else 0
+        fam.data = data.ctypes.data if data is not None else None
+        fam.theta = arr
+    desc.Mp = model.Mp.ctypes.data if model.Mp is not None else None
+    return desc, keep
+
+
 class DeviceModel:
-    """Operators of a :class:`ReducedModel` resident on one GPU (rbns_model_create)."""
+    """Operators of a :class:`ReducedModel` resident on one GPU (rbns_model_create2)."""
 
     def __init__(self, model: ReducedModel, device: int | torch.device = 0):
         self.lib = _native.load()
@@ -85,20 +106,11 @@ class DeviceModel:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.model = model
-        terms = (_native.ThetaTermC * max(1, model.q))()
-        for i, t in enumerate(model.theta):
-            terms[i] = _native.ThetaTermC(t.kind, t.k, t.m, 0, t.scale)
-        desc = _native.ModelDescC()
-        desc.n, desc.q, desc.n_p = model.n, model.q, model.n_p
-        desc.A = model.A.ctypes.data
-        desc.C = model.C.ctypes.data
-        desc.f = model.f.ctypes.data
-        desc.Mp = model.Mp.ctypes.data if model.Mp is not None else None
-        desc.Bq = model.Bq.ctypes.data if model.Bq is not None else None
-        desc.theta = terms
+        desc, keep = _native_desc(model)
         handle = ctypes.c_void_p()
-        _native.check(self.lib.rbns_model_create(ctypes.byref(desc), dev.index, ctypes.byref(handle)),
-                      "rbns_model_create")
+        _native.check(self.lib.rbns_model_create2(ctypes.byref(desc), dev.index, ctypes.byref(handle)),
+                      "rbns_model_create2")
+        self._keep = keep
         self._h = handle
 
     # -- lifecycle --------------------------------------------------------------------------------------
@@ -126,6 +138,12 @@ class DeviceModel:
     @property
     def n_p(self) -> int:
         return self.model.n_p
+
+    def terms(self) -> dict:
+        """Term plan of the device handle: family sizes, contraction blocks, h groups (rbns_model_terms)."""
+        c = (ctypes.c_int32 * 6)()
+        _native.check(self.lib.rbns_model_terms(self._h, c), "rbns_model_terms")
+        return dict(zip(("linear", "quadratic", "load", "coupling", "blocks", "groups"), list(c)))
 
     def device_bytes(self) -> int:
         return int(self.lib.rbns_model_device_bytes(self._h))

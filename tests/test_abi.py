@@ -37,7 +37,7 @@ def test_all_header_symbols_exported(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rbns_abi_version() == 1
+    assert lib.rbns_abi_version() == 2
     assert lib.rbns_error_string(0) == b"ok"
     assert b"invalid" in lib.rbns_error_string(1)
     assert lib.rbns_error_string(99) == b"unknown error"
@@ -52,8 +52,21 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     desc.n, desc.q = 0, 1
     assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
     assert b"N >= 1" in lib.rbns_last_error_message()
-    desc.n, desc.q = 10, 17
+    desc.n, desc.q = 10, 129
     assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
+    assert b"count outside" in lib.rbns_last_error_message()
+    desc.n, desc.q = 10, 2  # NULL operators
+    assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
+    assert b"NULL" in lib.rbns_last_error_message()
+    d2 = _native.ModelDesc2C()
+    d2.n = 10
+    assert lib.rbns_model_create2(ctypes.byref(d2), 0, ctypes.byref(out)) == 1
+    assert b"linear family" in lib.rbns_last_error_message()
+    terms = (_native.ThetaTermC * 1)(_native.ThetaTermC(9, 0, 0, 0, 1.0))
+    a = (ctypes.c_double * 100)()
+    d2.linear.count, d2.linear.data, d2.linear.theta = 1, ctypes.addressof(a), terms
+    assert lib.rbns_model_create2(ctypes.byref(d2), 0, ctypes.byref(out)) == 1
+    assert b"bad theta descriptor" in lib.rbns_last_error_message()
     assert lib.rbns_solve(None, None, 0, 1e-12, 20, None, None, None, None, None, None) == 1
     assert lib.rbns_model_destroy(None) == 0
 
@@ -71,4 +84,6 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_native.ThetaTermC) == 24
     assert ctypes.sizeof(_native.ModelDescC) == 16 + 6 * 8
+    assert ctypes.sizeof(_native.TermFamilyC) == 24
+    assert ctypes.sizeof(_native.ModelDesc2C) == 16 + 4 * 24 + 8
     assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 40

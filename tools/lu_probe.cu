@@ -43,11 +43,14 @@ int main(int argc, char** argv) {
   for (int i = 0; i < B; ++i) { h[i] = i; hm[2 * i] = 0.3; hm[2 * i + 1] = 100.0; }
   cudaMemcpy(act, h.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice);
   cudaMemcpy(mu, hm.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice);
+  rbns_theta_term* thf;
+  cudaMalloc(&thf, sizeof(rbns_theta_term));
+  const rbns_theta_term one{RBNS_THETA_CONST, 0, 0, 0, 1.0};
+  cudaMemcpy(thf, &one, sizeof(one), cudaMemcpyHostToDevice);
   NewtonParams p{};
-  p.act = act; p.n = B; p.J = J; p.ldj = ldj; p.u = u; p.mu = mu; p.A = nullptr; p.f = f;
-  p.N = N; p.Q = 1; p.first = 0; p.iter = 1; p.max_iter = 100; p.tol = 1e-12;
+  p.act = act; p.n = B; p.J = J; p.ldj = ldj; p.u = u; p.mu = mu; p.f = f; p.thf = thf;
+  p.N = N; p.Qf = 1; p.G = 1; p.ge[0] = -1; p.iter = 1; p.max_iter = 100; p.tol = 1e-12;
   p.iters = iters; p.status = status; p.last = last;
-  p.th.q = 1; p.th.kind[0] = RBNS_THETA_CONST; p.th.scale[0] = 1.0;
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
   int sms = 0;
