@@ -14,10 +14,11 @@ deviation):
 from __future__ import annotations
 
 from dataclasses import dataclass
+from math import factorial
 
 import numpy as np
 
-from .affine import family
+from .affine import MONOMIAL, ThetaTerm, family
 from .model import ReducedModel
 
 
@@ -91,3 +92,66 @@ def config_mu(cfg: Config | int, batch: int | None = None) -> np.ndarray:
     cfg = CONFIGS[cfg] if isinstance(cfg, int) else cfg
     mu = make_mu(cfg.batch, cfg.re_max)
     return mu if batch is None else mu[:batch].copy()
+
+
+# ---- the paper's term structure (lifted, Piola formulation) ------------------------------------------------
+
+NU_PAPER = 1.0 / 6.0  # SPEC.md:237 "viscosity was set at ν = 1/6"
+
+
+def lifted_families(series: int, nu: float = NU_PAPER):
+    """Descriptor families of a lifted Piola model at series order n (§5.2):
+    linear = a-terms ν·φᵏ/k! (k = 0..4n+2) + c0-terms u∞·φᵏ/k! (k = 0..4n); quadratic = c-terms φᵏ/k!
+    (k = 0..4n); load = d0 viscous-lift u∞·φᵏ/k! (k = 0..4n+2) + lift-lift u∞²·φᵏ/k! (k = 0..4n).
+    μ = (φ, u∞); the 1/k! scales mirror the truncated rotation series the affine terms come from."""
+    ka, kc = 4 * series + 3, 4 * series + 1
+    lin = [ThetaTerm(MONOMIAL, k, 0, nu / factorial(k)) for k in range(ka)]
+    lin += [ThetaTerm(MONOMIAL, k, 1, 1.0 / factorial(k)) for k in range(kc)]
+    quad = [ThetaTerm(MONOMIAL, k, 0, 1.0 / factorial(k)) for k in range(kc)]
+    load = [ThetaTerm(MONOMIAL, k, 1, 1.0 / factorial(k)) for k in range(ka)]
+    load += [ThetaTerm(MONOMIAL, k, 2, 1.0 / factorial(k)) for k in range(kc)]
+    return lin, quad, load
+
+
+def make_lifted_model(n: int, series: int, seed: int = 0, nu: float = NU_PAPER, kappa_c: float = 5e-5,
+                      kappa_0: float = 1e-3, lift2: float = 0.05, n_p: int = 0,
+                      name: str = "lifted") -> ReducedModel:
+    """Seeded model with the paper's per-form families (no real reduced model ships with the reference; the
+    operator values are synthetic, the term structure and μ = (φ, u∞) rules are the paper's).
+
+    Generation order (PCG64 ``seed``): G → A_{k≥1} → c0 terms → C → f (u∞ family, then u∞²) [→ H → B].
+    A₀ = GGᵀ/N + I, A_{k≥1} = 0.1·sym(N(0,1))/√N; c0 terms κ₀·N(0,1)/√N (non-symmetric: c(ℓ,u,w)+c(u,ℓ,w));
+    C_c = κ_C·N(0,1)/N antisymmetrised in (k,l); u∞ loads N(0,1), u∞² loads lift2·N(0,1)."""
+    rng = np.random.default_rng(seed)
+    lin_t, quad_t, load_t = lifted_families(series, nu)
+    ka, kc = 4 * series + 3, 4 * series + 1
+    A = np.empty((ka + kc, n, n))
+    G = rng.standard_normal((n, n))
+    A[0] = G @ G.T / n + np.eye(n)
+    for i in range(1, ka):
+        S = rng.standard_normal((n, n))
+        A[i] = 0.1 * (S + S.T) / 2.0 / np.sqrt(n)
+    A[ka:] = kappa_0 * rng.standard_normal((kc, n, n)) / np.sqrt(n)
+    C = rng.standard_normal((kc, n, n, n))
+    C *= kappa_c / n
+    C = 0.5 * (C - C.transpose(0, 1, 3, 2))
+    f = np.concatenate([rng.standard_normal((ka, n)), lift2 * rng.standard_normal((kc, n))])
+    Mp = Bq = None
+    coupling = None
+    if n_p:
+        H = rng.standard_normal((n_p, n_p))
+        Mp = H @ H.T / n_p + np.eye(n_p)
+        Bq = rng.standard_normal((kc, n_p, n)) / np.sqrt(n)
+        coupling = quad_t
+    return ReducedModel(A=A, C=C, f=f, Mp=Mp, Bq=Bq, name=name, theta_linear=lin_t, theta_quadratic=quad_t,
+                        theta_load=load_t, theta_coupling=coupling, nu_linear=False,
+                        meta={"seed": seed, "series": series, "nu": nu, "kappa_c": kappa_c, "kappa_0": kappa_0,
+                              "lift2": lift2, "form": "lifted-piola"})
+
+
+def make_lifted_mu(batch: int, seed: int = 1, phi_max_deg: float = 35.0, uinf=(1.0, 20.0)) -> np.ndarray:
+    """μ[b] = (φ [rad], u∞): φ ~ U[−35°, 35°], u∞ ~ U[1, 20] (the paper's parameter box)."""
+    rng = np.random.default_rng(seed)
+    phi = rng.uniform(-np.deg2rad(phi_max_deg), np.deg2rad(phi_max_deg), batch)
+    u = rng.uniform(uinf[0], uinf[1], batch)
+    return np.ascontiguousarray(np.stack([phi, u], axis=1))

@@ -14,6 +14,9 @@
    (assemble.py:86-101 docstring: "the Newton Jacobian block is their sum, the residual contribution N1 @ coeffs").
 2. ``synthetic_cfg{0..4}.npz`` — seeded BASELINE.json configs (SURVEY.md Appendix B pins): μ slices, oracle
    velocity/pressure, Newton counts and statuses, plus operator checksums that detect generator drift.
+3. ``lifted_small.npz`` / ``lifted_n12.npz`` — seeded models with the paper's per-form term families
+   (synthetic.make_lifted_model: a + c0 linear, c quadratic, d0 u∞/u∞² loads; μ = (φ, u∞)), the small one with
+   pressure recovery on its own coupling family.
 """
 
 from __future__ import annotations
@@ -136,6 +139,25 @@ def synthetic_fixtures() -> None:
         print(f"synthetic_cfg{c}.npz: B={nb} iters={np.bincount(data['iters']).tolist()}")
 
 
+LIFTED = {"lifted_small": dict(n=12, series=2, n_p=6, nb=64), "lifted_n12": dict(n=50, series=12, n_p=0, nb=8)}
+
+
+def lifted_fixtures() -> None:
+    for name, spec in LIFTED.items():
+        model = synthetic.make_lifted_model(spec["n"], spec["series"], n_p=spec["n_p"])
+        mu = synthetic.make_lifted_mu(spec["nb"])
+        res = [oracle.solve_sample(model, mu[b]) for b in range(spec["nb"])]
+        u = np.array([r[0] for r in res])
+        data = dict(mu=mu, u=u, iters=np.array([r[1] for r in res]), status=np.array([r[2] for r in res]),
+                    last=np.array([r[3] for r in res]), checksums=checksums(model))
+        if spec["n_p"]:
+            data["p"] = oracle.recover_pressure(model, mu, u)
+        np.savez_compressed(HERE / f"{name}.npz", **data)
+        print(f"{name}.npz: B={spec['nb']} iters={np.bincount(data['iters']).tolist()}")
+
+
 if __name__ == "__main__":
-    reference_operator_fixture()
-    synthetic_fixtures()
+    if "--lifted" not in sys.argv:
+        reference_operator_fixture()
+        synthetic_fixtures()
+    lifted_fixtures()
