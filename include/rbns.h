@@ -31,7 +31,7 @@ extern "C" {
 #endif
 
 #define RBNS_ABI_VERSION 2
-#define RBNS_MAX_TERMS 128 /* per term family */
+#define RBNS_MAX_TERMS 256 /* per term family */
 #define RBNS_MAX_GROUPS 4  /* distinct mu1 powers tying linear terms to the quadratic blocks (see create2) */
 
 /* θ_q(μ) descriptor kinds; μ = (mu0, mu1) = (alpha [rad], Re) for the BASELINE configs, (φ [rad], u∞) for the
@@ -92,8 +92,10 @@ typedef struct rbns_term_family {
 } rbns_term_family;
 
 enum rbns_model_flags {
-  RBNS_NU_LINEAR = 1 /* multiply the linear family by nu = 1/mu1 (BASELINE configs); clear for the paper's
-                        models, whose a-term descriptors carry nu in their scale */
+  RBNS_NU_LINEAR = 1,   /* multiply the linear family by nu = 1/mu1 (BASELINE configs); clear for the paper's
+                           models, whose a-term descriptors carry nu in their scale */
+  RBNS_STOP_ABSOLUTE = 2 /* stop when ||delta_stop||_2 <= tol (the coupled solvers' rule) instead
+                            of ||delta_stop||_2 <= tol * ||u_stop||_2 (block rule) */
 };
 
 /* Reduced model with per-form families.  Residual and Jacobian:
@@ -108,7 +110,8 @@ typedef struct rbns_model_desc2 {
   int32_t n;                   /* reduced velocity dimension N                           */
   int32_t n_p;                 /* pressure dimension Np (0 = no recovery)                */
   int32_t flags;               /* rbns_model_flags                                       */
-  int32_t reserved;
+  int32_t n_stop;              /* leading unknowns in the stop norm, 0 = all N (coupled saddle systems:
+                                  the velocity block)                        */
   rbns_term_family linear;     /* count x N x N         (>= 1 term)                      */
   rbns_term_family quadratic;  /* count x N x N x N     C[j][k][l] = c(u_j, u_k, u_l)    */
   rbns_term_family load;       /* count x N                                              */

@@ -14,9 +14,10 @@ from .errors import NativeError
 
 LIB_PATH = Path(os.environ.get("RBNS_LIB", Path(__file__).resolve().parent / "librbns.so"))
 
-MAX_TERMS = 128
+MAX_TERMS = 256
 MAX_GROUPS = 4
 NU_LINEAR = 1
+STOP_ABSOLUTE = 2
 STATUS_NAMES = {0: "CONVERGED", 1: "NON_CONVERGED", 2: "SINGULAR_SYSTEM", 3: "SINGULAR_RECOVERY", 4: "NONFINITE"}
 
 # every symbol include/rbns.h declares (checked by tests/test_abi.py)
@@ -46,7 +47,7 @@ class TermFamilyC(ctypes.Structure):
 
 class ModelDesc2C(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("n_p", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("linear", TermFamilyC), ("quadratic", TermFamilyC),
+                ("n_stop", ctypes.c_int32), ("linear", TermFamilyC), ("quadratic", TermFamilyC),
                 ("load", TermFamilyC), ("coupling", TermFamilyC), ("Mp", ctypes.c_void_p)]
 
 

@@ -24,7 +24,7 @@ SIN_K = 2          # scale * sin(k α)
 COS_SIN_POW = 3    # scale * cos(α)^k * sin(α)^m
 MONOMIAL = 4       # scale * α^k * Re^m      (the paper's scale·φᵏ·u∞ᵐ)
 
-MAX_TERMS = 128    # RBNS_MAX_TERMS (per term family)
+MAX_TERMS = 256    # RBNS_MAX_TERMS (per term family)
 
 
 @dataclass(frozen=True)

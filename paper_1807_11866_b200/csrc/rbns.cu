@@ -131,6 +131,7 @@ struct rbns_model {
   int Qa = 0, Qc = 0, Qf = 0, Qp = 0;      // family sizes: linear, quadratic, load, coupling
   int G = 0, ge[RBNS_MAX_GROUPS] = {};     // h groups and their μ₁ exponents
   int nu_lin = 0;
+  int n_stop = 0, stop_abs = 0;            // stop norm over the leading n_stop unknowns; absolute or relative
   Operand vel, prs;
   double* f = nullptr;                     // [Qf][N]
   double* L = nullptr;                     // [Np][Np]
@@ -194,6 +195,8 @@ NewtonParams newton_params(const rbns_model* m) {
   p.Qf = m->Qf;
   p.G = m->G;
   for (int g = 0; g < RBNS_MAX_GROUPS; ++g) p.ge[g] = m->ge[g];
+  p.n_stop = m->n_stop;
+  p.stop_abs = m->stop_abs;
   return p;
 }
 
@@ -487,6 +490,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   *out = nullptr;
   std::string why;
   if (d->n < 1 || d->n_p < 0) return fail(RBNS_ERR_INVALID_ARGUMENT, "need N >= 1, Np >= 0");
+  if (d->n_stop < 0 || d->n_stop > d->n) return fail(RBNS_ERR_INVALID_ARGUMENT, "n_stop outside [0, N]");
   if (!valid_terms(d->linear, true, "linear", why) || !valid_terms(d->quadratic, true, "quadratic", why) ||
       !valid_terms(d->load, true, "load", why) || !valid_terms(d->coupling, true, "coupling", why))
     return fail(RBNS_ERR_INVALID_ARGUMENT, why);
@@ -543,6 +547,8 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   m->Qf = d->load.count;
   m->Qp = d->n_p > 0 ? d->coupling.count : 0;
   m->nu_lin = nu_lin;
+  m->n_stop = d->n_stop > 0 ? d->n_stop : d->n;
+  m->stop_abs = (d->flags & RBNS_STOP_ABSOLUTE) ? 1 : 0;
   m->G = int(ge.size());
   for (int g = 0; g < m->G; ++g) m->ge[g] = ge[g];
   m->Ne = (m->N + 3) / 4 * 4;  // κ stride per block (k4 sub-steps never straddle)

@@ -33,6 +33,8 @@ struct NewtonParams {
   int32_t N, Qf;
   int32_t G;                   // L(μ)u = Σ_g μ₁^{ge[g]} h_g   (G = 1, ge = −1: ν A(μ)u of the BASELINE configs)
   int32_t ge[RBNS_MAX_GROUPS];
+  int32_t n_stop;              // leading unknowns in the stop norm (N: all; the velocity block of coupled systems)
+  int32_t stop_abs;            // 1: ‖δ‖ ≤ tol (SPEC.md:513 coupled rule), 0: ‖δ‖ ≤ tol·‖u_new‖ (block rule)
   int32_t iter, max_iter;
   double tol;
   int32_t* iters;
@@ -278,18 +280,22 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
   __syncthreads();
 
   // δ_k = rhs[perm[k]] / piv[k];  ‖δ‖², ‖u + δ‖² (fixed-order block reduction: deterministic)
-  double d2 = 0.0, un2 = 0.0;
+  double d2 = 0.0, un2 = 0.0, o2 = 0.0;  // o2: unknowns outside the stop norm
   if (!sing) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
       const double unew = p.u[int64_t(b) * N + k] + x;
-      d2 = fma(x, x, d2);
-      un2 = fma(unew, unew, un2);
+      if (k < p.n_stop) {
+        d2 = fma(x, x, d2);
+        un2 = fma(unew, unew, un2);
+      } else {
+        o2 = fma(x, x, fma(unew, unew, o2));
+      }
     }
   }
   d2 = block_sum<NT>(d2, sh.red[0]);
   un2 = block_sum<NT>(un2, sh.red[1]);
-  const bool finite = isfinite(d2) && isfinite(un2);
+  const bool finite = !__syncthreads_or(!isfinite(o2)) && isfinite(d2) && isfinite(un2);
   if (!sing && finite) {
     for (int k = tid; k < N; k += NT) {
       const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1))
       st = RBNS_SINGULAR_SYSTEM;
     else if (!finite)
       st = RBNS_NONFINITE;
-    else if (sqrt(d2) <= p.tol * sqrt(un2))
+    else if (sqrt(d2) <= p.tol * (p.stop_abs ? 1.0 : sqrt(un2)))
       st = RBNS_CONVERGED;
     else if (p.iter >= p.max_iter)
       st = RBNS_NON_CONVERGED;

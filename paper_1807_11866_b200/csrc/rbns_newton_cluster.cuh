@@ -217,18 +217,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
           if (s == rhs_slot) sh.rhs[tr + TGR * r] = a[r][s];
     }
     __syncthreads();
-    double d2 = 0.0, un2 = 0.0;
+    double d2 = 0.0, un2 = 0.0, o2 = 0.0;  // o2: unknowns outside the stop norm
     if (!sing) {
       for (int k = tid; k < N; k += NT) {
         const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
         const double unew = p.u[int64_t(b) * N + k] + x;
-        d2 = fma(x, x, d2);
-        un2 = fma(unew, unew, un2);
+        if (k < p.n_stop) {
+          d2 = fma(x, x, d2);
+          un2 = fma(unew, unew, un2);
+        } else {
+          o2 = fma(x, x, fma(unew, unew, o2));
+        }
       }
     }
     d2 = block_sum<NT>(d2, sh.red[0]);
     un2 = block_sum<NT>(un2, sh.red[1]);
-    const bool finite = isfinite(d2) && isfinite(un2);
+    const bool finite = !__syncthreads_or(!isfinite(o2)) && isfinite(d2) && isfinite(un2);
     if (!sing && finite) {
       for (int k = tid; k < N; k += NT) {
         const double x = sh.rhs[sh.perm[k]] / sh.piv[k];
@@ -241,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
         st = RBNS_SINGULAR_SYSTEM;
       else if (!finite)
         st = RBNS_NONFINITE;
-      else if (sqrt(d2) <= p.tol * sqrt(un2))
+      else if (sqrt(d2) <= p.tol * (p.stop_abs ? 1.0 : sqrt(un2)))
         st = RBNS_CONVERGED;
       else if (p.iter >= p.max_iter)
         st = RBNS_NON_CONVERGED;

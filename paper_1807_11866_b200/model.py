@@ -50,6 +50,8 @@ class ReducedModel:
     theta_load: Optional[Sequence[ThetaTerm]] = None
     theta_coupling: Optional[Sequence[ThetaTerm]] = None
     nu_linear: bool = True
+    n_stop: int = 0                    # leading unknowns in the Newton stop norm (0: all N)
+    stop_absolute: bool = False        # ‖δ‖ ≤ tol (coupled rule) instead of ‖δ‖ ≤ tol·‖u‖
 
     def __post_init__(self):
         A = np.ascontiguousarray(self.A, dtype=np.float64)
@@ -90,6 +92,10 @@ class ReducedModel:
         if self.Bq is not None and counts["coupling"] < 1:
             raise ValueError("pressure recovery needs at least one coupling term")
         object.__setattr__(self, "nu_linear", bool(self.nu_linear))
+        object.__setattr__(self, "stop_absolute", bool(self.stop_absolute))
+        if not 0 <= int(self.n_stop) <= n:
+            raise ValueError(f"n_stop={self.n_stop} outside [0, {n}]")
+        object.__setattr__(self, "n_stop", int(self.n_stop))
         for arr in (A, C, f):
             arr.flags.writeable = False
 
@@ -105,6 +111,11 @@ class ReducedModel:
     @property
     def n_p(self) -> int:
         return 0 if self.Mp is None else self.Mp.shape[0]
+
+    @property
+    def stop_dim(self) -> int:
+        """Number of leading unknowns in the stop norm."""
+        return self.n_stop or self.n
 
     @property
     def counts(self) -> Tuple[int, int, int, int]:

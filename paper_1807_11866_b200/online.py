@@ -77,7 +77,9 @@ def _native_desc(model: ReducedModel):
     """rbns_model_desc2 for a model (per-family descriptors, include/rbns.h); returns (desc, keep-alive list)."""
     desc = _native.ModelDesc2C()
     desc.n, desc.n_p = model.n, model.n_p
-    desc.flags = _native.NU_LINEAR if model.nu_linear else 0
+    desc.flags = ((_native.NU_LINEAR if model.nu_linear else 0)
+                  | (_native.STOP_ABSOLUTE if model.stop_absolute else 0))
+    desc.n_stop = model.n_stop
     keep = []
     fams = (("linear", model.A), ("quadratic", model.C), ("load", model.f), ("coupling", model.Bq))
     for name, data in fams:

@@ -53,7 +53,7 @@ def _json_safe(meta: dict) -> dict:
     return out
 
 
-def _digest(arrays: Dict[str, np.ndarray], families: dict, nu_linear: bool) -> str:
+def _digest(arrays: Dict[str, np.ndarray], families: dict, nu_linear: bool, stop: dict) -> str:
     h = hashlib.sha256()
     for name in sorted(arrays):
         a = arrays[name]
@@ -62,6 +62,7 @@ def _digest(arrays: Dict[str, np.ndarray], families: dict, nu_linear: bool) -> s
         h.update(np.ascontiguousarray(a, dtype="<f8").tobytes())
     h.update(json.dumps(families, sort_keys=True).encode())
     h.update(b"nu_linear" if nu_linear else b"nu_none")
+    h.update(json.dumps(stop, sort_keys=True).encode())
     return h.hexdigest()
 
 
@@ -91,10 +92,11 @@ def save_model(model: ReducedModel, path: os.PathLike) -> Path:
         "basis": {"n_velocity": model.n, "n_pressure": model.n_p},
         "viscosity": "nu = 1/mu1 multiplies the linear family" if model.nu_linear else "in the descriptors",
         "nu_linear": model.nu_linear,
+        "stop": {"n_stop": model.n_stop, "absolute": model.stop_absolute},
         "families": families,
         "arrays": records,
         "provenance": _json_safe(model.meta),
-        "hash": _digest(arrays, families, model.nu_linear),
+        "hash": _digest(arrays, families, model.nu_linear, {"n_stop": model.n_stop, "absolute": model.stop_absolute}),
     }
     text = json.dumps(manifest, sort_keys=True, indent=1) + "\n"
     (path / "manifest.json").write_text(text)
@@ -142,14 +144,16 @@ def load_model(path: os.PathLike, mmap: bool = False) -> ReducedModel:
         thetas = {fam: [ThetaTerm(int(t["kind"]), int(t["k"]), int(t["m"]), float.fromhex(t["scale_hex"]))
                         for t in rec["terms"]] for fam, rec in fams.items()}
         nu_linear = bool(man["nu_linear"])
+        stop = man.get("stop", {"n_stop": 0, "absolute": False})
     except (KeyError, TypeError, ValueError) as exc:
         raise StoreError(f"{mf}: inconsistent manifest ({exc})") from exc
-    if _digest(arrays, fams, nu_linear) != man.get("hash"):
+    if _digest(arrays, fams, nu_linear, stop) != man.get("hash"):
         raise StoreError(f"{mf}: provenance hash mismatch")
     try:
         return ReducedModel(A=arrays["A"], C=arrays["C"], f=arrays["f"], Mp=arrays.get("Mp"), Bq=arrays.get("Bq"),
                             name=man.get("name", "reduced-model"), meta=dict(man.get("provenance", {})),
                             theta_linear=thetas["linear"], theta_quadratic=thetas["quadratic"],
-                            theta_load=thetas["load"], theta_coupling=thetas.get("coupling"), nu_linear=nu_linear)
+                            theta_load=thetas["load"], theta_coupling=thetas.get("coupling"), nu_linear=nu_linear,
+                            n_stop=int(stop["n_stop"]), stop_absolute=bool(stop["absolute"]))
     except (KeyError, ValueError) as exc:
         raise StoreError(f"{path}: arrays inconsistent with the families ({exc})") from exc

@@ -155,3 +155,44 @@ def make_lifted_mu(batch: int, seed: int = 1, phi_max_deg: float = 35.0, uinf=(1
     phi = rng.uniform(-np.deg2rad(phi_max_deg), np.deg2rad(phi_max_deg), batch)
     u = rng.uniform(uinf[0], uinf[1], batch)
     return np.ascontiguousarray(np.stack([phi, u], axis=1))
+
+
+def make_coupled_model(m: int, series: int, stabilized: bool = True, seed: int = 0, kappa_s: float = 0.1):
+    """Saddle-system blocks for the naive coupled solvers around the lifted velocity model
+    ``make_lifted_model(m, series, seed)`` — its (A, C, f) are the velocity-velocity blocks verbatim.
+
+    Div-conforming structure (Eq. (piolablock)): the velocity modes are solenoidal, so the
+    velocity-pressure block B_pu is exactly zero; the supremizer-pressure block B_ps (Np = m) is regular.
+    Stabilised (v = (u, s), size 3m): extra supremizer blocks A_us, A_su, A_ss (A_ss[0] = HHᵀ/m + I), mixed
+    convective entries κ_C-sized, supremizer loads f_s; b-terms φᵏ/k! (k = 0..4n) with B_ps[0] = I + 0.3·G/√m.
+    Unstabilised (v = u, size 2m): B = B_pu = 0 — the machine-zero inf-sup case that must fail gracefully.
+    Returns (CoupledModel, the block ReducedModel)."""
+    from .coupled import CoupledModel
+
+    block = make_lifted_model(m, series, seed=seed)
+    lin_t, quad_t, load_t = block.theta_linear, block.theta_quadratic, block.theta_load
+    qa, qc, qf = block.counts[:3]
+    div_t = [ThetaTerm(MONOMIAL, k, 0, 1.0 / factorial(k)) for k in range(4 * series + 1)]
+    rng = np.random.default_rng(seed + 1000)
+    if not stabilized:
+        return CoupledModel(A=block.A, B=np.zeros((len(div_t), m, m)), C=block.C, f=block.f, theta_linear=lin_t,
+                            theta_div=div_t, theta_quadratic=quad_t, theta_load=load_t, nu_linear=False,
+                            stabilized=False, name=f"coupled-2M-{m}"), block
+    nv = 2 * m
+    A = np.zeros((qa, nv, nv))
+    A[:, :m, :m] = block.A
+    A[:, :m, m:] = kappa_s * rng.standard_normal((qa, m, m)) / np.sqrt(m) * 0.1
+    A[:, m:, :m] = A[:, :m, m:].transpose(0, 2, 1)
+    H = rng.standard_normal((m, m))
+    A[0, m:, m:] = H @ H.T / m + np.eye(m)
+    A[1:, m:, m:] = 0.1 * kappa_s * rng.standard_normal((qa - 1, m, m)) / np.sqrt(m)
+    kc = block.meta["kappa_c"]
+    C = rng.standard_normal((qc, nv, nv, nv)) * (kc / nv)
+    C = 0.5 * (C - C.transpose(0, 1, 3, 2))
+    C[:, :m, :m, :m] = block.C
+    f = np.concatenate([block.f, rng.standard_normal((qf, m))], axis=1)
+    B = np.zeros((len(div_t), m, nv))
+    B[:, :, m:] = 0.1 * rng.standard_normal((len(div_t), m, m)) / np.sqrt(m)
+    B[0, :, m:] = np.eye(m) + 0.3 * rng.standard_normal((m, m)) / np.sqrt(m)
+    return CoupledModel(A=A, B=B, C=C, f=f, theta_linear=lin_t, theta_div=div_t, theta_quadratic=quad_t,
+                        theta_load=load_t, nu_linear=False, stabilized=True, name=f"coupled-3M-{m}"), block

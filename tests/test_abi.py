@@ -52,7 +52,7 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     desc.n, desc.q = 0, 1
     assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
     assert b"N >= 1" in lib.rbns_last_error_message()
-    desc.n, desc.q = 10, 129
+    desc.n, desc.q = 10, 257
     assert lib.rbns_model_create(ctypes.byref(desc), 0, ctypes.byref(out)) == 1
     assert b"count outside" in lib.rbns_last_error_message()
     desc.n, desc.q = 10, 2  # NULL operators

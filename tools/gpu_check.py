@@ -40,7 +40,7 @@ def timing(c, nb=None, reps=3):
             fl = s['contraction_iterations'] * 2 * cfg.q * cfg.n**3
             print(f"cfg{c} B={len(mu)}: {dt*1e3:.1f} ms, {len(mu)/dt:.0f} solves/s, gemm {s['ms_gemm']:.1f} ms ({fl/s['ms_gemm']/1e9:.1f} TF/s), lu {s['ms_lu']:.1f} ms, rec {s['ms_recovery']:.1f} ms, total {s['ms_total']:.1f}, sample_it {s['sample_iterations']}", flush=True)
 
-if __name__ == "__main__" and "lifted" not in sys.argv:
+if __name__ == "__main__" and not {"lifted", "coupled"} & set(sys.argv):
     check(0, 64)
     check(1, 512)
     check(2, 256)
@@ -71,3 +71,17 @@ def lifted_timing(n=50, series=12, nb=65536, reps=2):
 
 if __name__ == "__main__" and "lifted" in sys.argv:
     lifted_timing()
+
+def coupled_timing(m=50, series=12, nb=16384):
+    """Block (velocity-only, size M) vs naive coupled-3M on the same lifted model."""
+    from paper_1807_11866_b200.coupled import solve_coupled_batch
+    cm, blk = synthetic.make_coupled_model(m, series)
+    mu = synthetic.make_lifted_mu(nb)
+    dm = online.device_model(blk)
+    dm.solve_host(mu); solve_coupled_batch(cm, mu)
+    for name, fn in (("block", lambda: dm.solve_host(mu)), ("coupled-3M", lambda: solve_coupled_batch(cm, mu))):
+        torch.cuda.synchronize(); t = time.perf_counter(); r = fn(); torch.cuda.synchronize(); dt = time.perf_counter() - t
+        print(f"{name} M={m} B={nb}: {dt*1e3:.1f} ms, {nb/dt:.0f} solves/s", flush=True)
+
+if __name__ == "__main__" and "coupled" in sys.argv:
+    coupled_timing()

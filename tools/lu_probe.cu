@@ -49,7 +49,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(thf, &one, sizeof(one), cudaMemcpyHostToDevice);
   NewtonParams p{};
   p.act = act; p.n = B; p.J = J; p.ldj = ldj; p.u = u; p.mu = mu; p.f = f; p.thf = thf;
-  p.N = N; p.Qf = 1; p.G = 1; p.ge[0] = -1; p.iter = 1; p.max_iter = 100; p.tol = 1e-12;
+  p.N = N; p.Qf = 1; p.G = 1; p.ge[0] = -1; p.n_stop = N; p.stop_abs = 0; p.iter = 1; p.max_iter = 100; p.tol = 1e-12;
   p.iters = iters; p.status = status; p.last = last;
   int clk_khz = 0;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
