@@ -14,6 +14,10 @@
    (assemble.py:86-101 docstring: "the Newton Jacobian block is their sum, the residual contribution N1 @ coeffs").
 2. ``synthetic_cfg{0..4}.npz`` — seeded BASELINE.json configs (SURVEY.md Appendix B pins): μ slices, oracle
    velocity/pressure, Newton counts and statuses, plus operator checksums that detect generator drift.
+4. ``projection_ref.npz`` — reduced-basis tabulations at the quadrature points of a small deformed mesh (from the
+   reference's ``deformed_tables`` / ``field_at_quadrature``) and the reference's own projected operators
+   V_lᵀ N1(V_j) V_k and Vᵀ A_h V (``convection_matrices`` / ``viscous_matrix`` + sparse products): the pin for
+   the GPU projection (paper_1807_11866_b200/projection.py).
 3. ``lifted_small.npz`` / ``lifted_n12.npz`` — seeded models with the paper's per-form term families
    (synthetic.make_lifted_model: a + c0 linear, c quadratic, d0 u∞/u∞² loads; μ = (φ, u∞)), the small one with
    pressure recovery on its own coupling family.
@@ -156,8 +160,40 @@ def lifted_fixtures() -> None:
         print(f"{name}.npz: B={spec['nb']} iters={np.bincount(data['iters']).tolist()}")
 
 
+def projection_fixture(m: int = 6, seed: int = 11) -> None:
+    sys.path.insert(0, str(REF_SRC))
+    from rbflow import assemble, geometry, spaces  # the reference package (read-only import)
+
+    prof = geometry.naca_profile(0.15, 12)
+    mesh = geometry.build_omesh(prof, 6.0, 12, 4, 1.2)
+    space = spaces.build_space_pair(mesh, spaces.DIV_CONFORMING)
+    geom = geometry.DeformedGeometry()
+    rng = np.random.default_rng(seed)
+    V = np.zeros((space.n_vdofs, m))
+    Qm, _ = np.linalg.qr(rng.standard_normal((space.free_v.size, m)))
+    V[space.free_v] = Qm
+    dval, dgrad = assemble.deformed_tables(space, geom, math.radians(20.0), "piola")
+    vals, grads = [], []
+    for j in range(m):
+        v, g = assemble.field_at_quadrature(space, dval, dgrad, V[:, j])   # (nel,nq,2), (nel,nq,2,2)
+        vals.append(v.reshape(-1, 2)), grads.append(g.reshape(-1, 2, 2))
+    val = np.stack(vals, axis=-1)                                            # (P, 2, m)
+    grad = np.stack(grads, axis=-1)                                          # (P, 2, 2, m): [c, d] = ∂_d u_c
+    w = space.qp_w.reshape(-1)
+    C = np.empty((m, m, m))
+    for j in range(m):
+        N1, _ = assemble.convection_matrices(space, dval, dgrad, V[:, j])
+        C[j] = (V.T @ (N1 @ V)).T                                            # C[j,k,l] = V_lᵀ N1(V_j) V_k
+    A = V.T @ (assemble.viscous_matrix(space, dgrad, 1.0) @ V)
+    np.savez_compressed(HERE / "projection_ref.npz", val=val, grad=grad, w=w, C_ref=C, A_ref=A,
+                        mesh=np.array([12, 4]), phi=math.radians(20.0))
+    print("projection_ref.npz: P", val.shape[0], "m", m, "|C|", np.abs(C).max(), "|A|", np.abs(A).max())
+
+
 if __name__ == "__main__":
-    if "--lifted" not in sys.argv:
+    if "--lifted" not in sys.argv and "--projection" not in sys.argv:
         reference_operator_fixture()
         synthetic_fixtures()
-    lifted_fixtures()
+    if "--projection" not in sys.argv:
+        lifted_fixtures()
+    projection_fixture()
