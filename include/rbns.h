@@ -134,6 +134,8 @@ typedef struct rbns_stats {
   double ms_recovery;             /* device time in pressure recovery                             */
   double ms_total;                /* device time of the whole call (excluding host copies)        */
   double ms_assembly;             /* device time of the u = 0 step's affine assembly (J = nu A(mu)) */
+  int64_t pivot_fallbacks;        /* sample-iterations whose pivot-order hint failed verification and
+                                     ran the full-search factorization                               */
 } rbns_stats;
 
 /* Copy operators to `device`, build the symmetrised GEMM operand S_q = C_q + C_q^(12),

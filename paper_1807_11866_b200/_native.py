@@ -56,7 +56,8 @@ class StatsC(ctypes.Structure):
                 ("newton_rounds", ctypes.c_int32), ("kernel_launches", ctypes.c_int32),
                 ("gemm_launches", ctypes.c_int32), ("lu_launches", ctypes.c_int32),
                 ("ms_gemm", ctypes.c_double), ("ms_lu", ctypes.c_double), ("ms_recovery", ctypes.c_double),
-                ("ms_total", ctypes.c_double), ("ms_assembly", ctypes.c_double)]
+                ("ms_total", ctypes.c_double), ("ms_assembly", ctypes.c_double),
+                ("pivot_fallbacks", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

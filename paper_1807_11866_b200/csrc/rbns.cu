@@ -202,6 +202,7 @@ NewtonParams newton_params(const rbns_model* m) {
 
 int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
                   const double* mu, int iter, int max_iter, double tol, int32_t* iters, int8_t* status, double* last,
+                  int16_t* hints, int32_t* spec_miss, int32_t* miss_list, int32_t* miss_count, int* launches,
                   cudaStream_t st) {
   if (n <= 0) return RBNS_OK;
   NewtonParams p = newton_params(m);
@@ -217,7 +218,12 @@ int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int
   p.iters = iters;
   p.status = status;
   p.last = last;
-  RBNS_CUDA(launch_newton_update(p, st));
+  p.hint_in = iter > 1 ? hints : nullptr;  // the first iteration starts from the identity order
+  p.hint_out = hints;
+  p.spec_miss = spec_miss;
+  p.miss_list = miss_list;
+  p.miss_count = miss_count;
+  RBNS_CUDA(launch_newton_update(p, st, launches));
   return RBNS_OK;
 }
 
@@ -310,15 +316,20 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
 
   const int64_t ldj = m->vel.row_tiles * kBN;
   int32_t *act0 = nullptr, *act1 = nullptr, *dcount = nullptr;
+  int16_t* hints = nullptr;  // per-sample pivot order of the previous Newton iteration (speculation hint)
   RBNS_CUDA(cudaMallocAsync(&act0, size_t(B) * sizeof(int32_t), st));
   RBNS_CUDA(cudaMallocAsync(&act1, size_t(B) * sizeof(int32_t), st));
-  RBNS_CUDA(cudaMallocAsync(&dcount, sizeof(int32_t), st));
+  RBNS_CUDA(cudaMallocAsync(&dcount, 3 * sizeof(int32_t), st));  // active count, hint misses, chunk misses
+  RBNS_CUDA(cudaMallocAsync(&hints, size_t(B) * m->N * sizeof(int16_t), st));
+  RBNS_CUDA(cudaMemsetAsync(dcount, 0, 3 * sizeof(int32_t), st));
   const int64_t budget = env_int64("RBNS_JBUF_BYTES", int64_t(8) << 30);
   const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldj * 8)));
+  int32_t* miss_list = nullptr;  // chunk positions whose pivot hint failed (re-run by the exact kernel)
+  RBNS_CUDA(cudaMallocAsync(&miss_list, size_t(std::max<int64_t>(1, std::min<int64_t>(B, cap))) * sizeof(int32_t), st));
   double* jbuf = nullptr;
   if (max_iter > 0) RBNS_CUDA(cudaMallocAsync(&jbuf, size_t(cap) * ldj * sizeof(double), st));
   static thread_local int32_t* hcount = nullptr;
-  if (!hcount) RBNS_CUDA(cudaMallocHost(&hcount, sizeof(int32_t)));
+  if (!hcount) RBNS_CUDA(cudaMallocHost(&hcount, 2 * sizeof(int32_t)));
 
   init_solve<<<grid_for(B, 256), 256, 0, st>>>(act0, status, iters, last, B);
   RBNS_CUDA(cudaMemsetAsync(u, 0, size_t(B) * m->N * sizeof(double), st));
@@ -346,11 +357,13 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
         stats.kernel_launches += 1;
       }
       const int e = timer.begin(1);
-      rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, st);
+      int nl = 0;
+      rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, hints,
+                         dcount + 1, miss_list, dcount + 2, &nl, st);
       timer.end(e);
       if (rc) break;
-      stats.lu_launches += 1;
-      stats.kernel_launches += 1;
+      stats.lu_launches += nl;
+      stats.kernel_launches += nl;
     }
     if (rc) break;
     compact_active<<<1, kCompactThreads, 0, st>>>(act0, int32_t(n_act), status, act1, dcount);
@@ -371,6 +384,9 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     }
   }
   cudaEventRecord(t1, st);
+  if (rc == RBNS_OK) RBNS_CUDA(cudaMemcpyAsync(hcount + 1, dcount + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(hints, st);
+  cudaFreeAsync(miss_list, st);
   cudaFreeAsync(act0, st);
   cudaFreeAsync(act1, st);
   cudaFreeAsync(dcount, st);
@@ -385,6 +401,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     stats.ms_lu = timer.total(1);
     stats.ms_recovery = timer.total(2);
     stats.ms_assembly = timer.total(3);
+    stats.pivot_fallbacks = hcount[1];
     std::lock_guard<std::mutex> lk(m->stats_mu);
     m->stats = stats;
   }

@@ -10,6 +10,7 @@ namespace rbns {
 struct NewtonParams;
 
 bool newton_supported(int N);
-cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st);
+// launches the Newton-update kernel(s) for p on st; *launches receives the number of kernels launched
+cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches);
 
 }  // namespace rbns

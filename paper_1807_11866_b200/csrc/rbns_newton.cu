@@ -8,6 +8,8 @@
 #include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
 #include "rbns_newton2.cuh"
+#include "rbns_newton3.cuh"
+#include "rbns_newton_spec.cuh"
 #include "rbns_newton_cluster.cuh"
 
 namespace rbns {
@@ -18,15 +20,27 @@ using NewtonKernel = void (*)(const NewtonParams);
 struct Shape {
   int tgr, tgc, rs, cs;
   NewtonKernel kern;
+  NewtonKernel exact = nullptr;  // speculative kernels: the full-search kernel for the samples they hand back
 };
 
+#define RBNS_SPEC(R_, C_, RS_, CS_) {R_, C_, RS_, CS_, newton_gjs_kernel<R_, C_, RS_, CS_>, newton_gj2_kernel<R_, C_, RS_, CS_>}
 const Shape kShapes[] = {
-    {4, 8, 4, 3, newton_gj2_kernel<4, 8, 4, 3>},       // N ≤ 16   (1 warp)
-    {4, 8, 8, 5, newton_gj2_kernel<4, 8, 8, 5>},       // N ≤ 32   (1 warp)
-    {4, 8, 13, 7, newton_gj2_kernel<4, 8, 13, 7>},     // N ≤ 52   (1 warp)
-    {8, 16, 10, 6, newton_gj2_kernel<8, 16, 10, 6>},   // N ≤ 80   (4 warps)
-    {8, 16, 13, 7, newton_gj2_kernel<8, 16, 13, 7>},   // N ≤ 104  (4 warps)
-    {16, 16, 8, 8, newton_gj2_kernel<16, 16, 8, 8>},   // N ≤ 127  (8 warps)
+    RBNS_SPEC(4, 8, 4, 3),     // N ≤ 16   (1 warp)
+    RBNS_SPEC(4, 8, 8, 5),     // N ≤ 32   (1 warp)
+    RBNS_SPEC(4, 8, 13, 7),    // N ≤ 52   (1 warp)
+    RBNS_SPEC(8, 16, 10, 6),   // N ≤ 80   (4 warps)
+    RBNS_SPEC(8, 16, 13, 7),   // N ≤ 104  (4 warps)
+    RBNS_SPEC(16, 16, 8, 8),   // N ≤ 127  (8 warps)
+};
+#undef RBNS_SPEC
+// RBNS_NEWTON=gj2: full pivot search every step (rbns_newton2.cuh) — also the speculative kernel's fallback
+const Shape kShapes2[] = {
+    {4, 8, 4, 3, newton_gj2_kernel<4, 8, 4, 3>},
+    {4, 8, 8, 5, newton_gj2_kernel<4, 8, 8, 5>},
+    {4, 8, 13, 7, newton_gj2_kernel<4, 8, 13, 7>},
+    {8, 16, 10, 6, newton_gj2_kernel<8, 16, 10, 6>},
+    {8, 16, 13, 7, newton_gj2_kernel<8, 16, 13, 7>},
+    {16, 16, 8, 8, newton_gj2_kernel<16, 16, 8, 8>},
 };
 // RBNS_NEWTON=gj1: the earlier owner-serial pivot search (rbns_newton.cuh), kept for comparison
 const Shape kShapes1[] = {
@@ -36,6 +50,16 @@ const Shape kShapes1[] = {
     {8, 16, 10, 6, newton_gj_kernel<8, 16, 10, 6>},
     {8, 16, 13, 7, newton_gj_kernel<8, 16, 13, 7>},
     {16, 16, 8, 8, newton_gj_kernel<16, 16, 8, 8>},
+};
+
+// RBNS_NEWTON=gj3: one barrier per step, redundant per-warp search, pivot row by warp shuffles (rbns_newton3.cuh)
+const Shape kShapes3[] = {
+    {4, 8, 4, 3, newton_gj3_kernel<4, 8, 4, 3>},
+    {4, 8, 8, 5, newton_gj3_kernel<4, 8, 8, 5>},
+    {4, 8, 13, 7, newton_gj3_kernel<4, 8, 13, 7>},
+    {8, 16, 10, 6, newton_gj3_kernel<8, 16, 10, 6>},
+    {8, 16, 13, 7, newton_gj3_kernel<8, 16, 13, 7>},
+    {16, 16, 8, 8, newton_gj3_kernel<16, 16, 8, 8>},
 };
 
 // RBNS_GJ_WIDE=1: 8 warps (16×16 grid, 49 register doubles per thread, two CTAs per SM) for 52 < N ≤ 112
@@ -50,9 +74,11 @@ const Shape* plan(int N) {
   static const int variant = [] {
     const char* v = std::getenv("RBNS_NEWTON");
     if (v && std::strcmp(v, "gj1") == 0) return 1;
-    return 2;
+    if (v && std::strcmp(v, "gj3") == 0) return 3;
+    if (v && std::strcmp(v, "gj2") == 0) return 2;
+    return 0;
   }();
-  const Shape* table = variant == 1 ? kShapes1 : kShapes;
+  const Shape* table = variant == 1 ? kShapes1 : variant == 2 ? kShapes2 : variant == 3 ? kShapes3 : kShapes;
   for (int i = 0; i < int(sizeof(kShapes) / sizeof(kShapes[0])); ++i) {
     const Shape& s = table[i];
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
@@ -98,7 +124,8 @@ constexpr int kClusterMaxN = 207;
 
 bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
 
-cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
+cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches) {
+  *launches = 1;
   if (use_blocked()) {
     if (const BShape* b = bplan(p.N)) {
       static bool attr_set[sizeof(kBShapes) / sizeof(kBShapes[0])] = {};
@@ -123,7 +150,19 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st) {
   if (!set1) { cudaFuncSetAttribute(s->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024); set1 = true; }
   s->kern<<<p.n, s->tgr * s->tgc, 150 * 1024, st>>>(p);
 #else
-  s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
+  if (s->exact) {
+    // speculative pass, then the exact kernel over the samples it handed back (device-side count)
+    cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
+    NewtonParams q = p;
+    q.sub = p.miss_list;
+    q.n_sub = p.miss_count;
+    s->exact<<<p.n, s->tgr * s->tgc, 0, st>>>(q);
+    *launches = 2;
+  } else {
+    s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
+  }
 #endif
   return cudaGetLastError();
 }

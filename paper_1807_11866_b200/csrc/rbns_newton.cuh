@@ -40,7 +40,20 @@ struct NewtonParams {
   int32_t* iters;
   int8_t* status;
   double* last;
+  const int16_t* hint_in;      // [B][N] pivot order hint (previous Newton iteration); NULL = identity
+  int16_t* hint_out;           // [B][N] pivot order chosen (may alias hint_in); NULL = not recorded
+  int32_t* spec_miss;          // count of CTAs whose hint failed verification (statistics), or NULL
+  int32_t* miss_list;          // speculative kernel: chunk positions whose hint failed (appended), or NULL
+  int32_t* miss_count;         //   … and their number (device counter, zeroed per chunk)
+  const int32_t* sub;          // exact kernels: run only the chunk positions sub[0 .. *n_sub) (NULL: all n)
+  const int32_t* n_sub;
 };
+
+// CTA → chunk position (and whether this CTA has work) for the exact kernels' optional subset launch
+__device__ __forceinline__ int newton_position(const NewtonParams& p) {
+  if (p.sub) return int(blockIdx.x) < *p.n_sub ? p.sub[blockIdx.x] : -1;
+  return int(blockIdx.x) < p.n ? int(blockIdx.x) : -1;
+}
 
 // Per-sample residual weights, evaluated once per CTA into shared memory.
 struct NewtonWeights {

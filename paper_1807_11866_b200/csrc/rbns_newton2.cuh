@@ -279,8 +279,8 @@ template <int TGR, int TGC, int RS, int CS, int MODE = 0>
 __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_gj2_kernel(const NewtonParams p) {
   static_assert(RS <= 32 && TGR <= 32 && TGC <= 32 && (TGR * TGC) % 32 == 0, "shape");
   __shared__ GJ2Shared<TGR, TGC, RS, CS> sh;
-  const int i_s = blockIdx.x;
-  if (i_s >= p.n) return;
+  const int i_s = newton_position(p);
+  if (i_s < 0) return;
   const int b = p.act[i_s];
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   double a[RS][CS];
@@ -288,6 +288,9 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
   bool sing = false;
   gj2_block<TGR, TGC, RS, CS, 0, MODE>(a, sing, p.N, tr, tc, sh);
   gj_finish<TGR, TGC, RS, CS>(p, b, a, sing, sh);
+  if (p.hint_out && !sing) {  // the order partial pivoting chose: the next iteration's speculation hint
+    for (int i = tid; i < p.N; i += TGR * TGC) p.hint_out[int64_t(b) * p.N + i] = int16_t(sh.perm[i]);
+  }
 }
 
 }  // namespace rbns

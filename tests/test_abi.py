@@ -86,4 +86,4 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.ModelDescC) == 16 + 6 * 8
     assert ctypes.sizeof(_native.TermFamilyC) == 24
     assert ctypes.sizeof(_native.ModelDesc2C) == 16 + 4 * 24 + 8
-    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 40
+    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 40 + 8

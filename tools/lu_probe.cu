@@ -7,6 +7,8 @@
 
 #include "rbns_newton.cuh"
 #include "rbns_newton2.cuh"
+#include "rbns_newton3.cuh"
+#include "rbns_newton_spec.cuh"
 
 using namespace rbns;
 
@@ -19,6 +21,11 @@ __global__ void fill(double* x, size_t n, unsigned seed) {
 }
 
 using K = void (*)(const NewtonParams);
+
+__global__ void add_diag(double* J, int64_t ldj, int N, int B, double d) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(B) * N; i += int64_t(gridDim.x) * blockDim.x)
+    J[(i / N) * ldj + (i % N) * (N + 1)] += d;
+}
 
 int main(int argc, char** argv) {
   const int N = argc > 1 ? atoi(argv[1]) : 100;
@@ -64,12 +71,33 @@ int main(int argc, char** argv) {
       {"gj2 -publish", newton_gj2_kernel<8, 16, 13, 7, 4>, 128},
       {"gj2 -update-search", newton_gj2_kernel<8, 16, 13, 7, 3>, 128},
       {"gj2 -all", newton_gj2_kernel<8, 16, 13, 7, 7>, 128},
+      {"gj3", newton_gj3_kernel<8, 16, 13, 7>, 128},
+      {"gjs (random J: hint misses)", newton_gjs_kernel<8, 16, 13, 7>, 128},
+  };
+  const V vd[] = {
+      {"gj2 (dominant J)", newton_gj2_kernel<8, 16, 13, 7, 0>, 128},
+      {"gjs (dominant J: hint hits)", newton_gjs_kernel<8, 16, 13, 7>, 128},
+      {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
+      {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
+      {"gj1 wide 16x16 (dominant J)", newton_gj_kernel<16, 16, 7, 7>, 256},
   };
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (const V& v : vs) {
+  int32_t* miss;
+  cudaMallocManaged(&miss, sizeof(int32_t));
+  p.spec_miss = miss;
+  int32_t *mlist, *mcount;
+  cudaMalloc(&mlist, sizeof(int32_t) * B);
+  cudaMallocManaged(&mcount, sizeof(int32_t));
+  p.miss_list = mlist;
+  p.miss_count = mcount;
+  auto run = [&](const V& v) {
+    *miss = 0;
+    *mcount = 0;
     v.k<<<B, v.threads>>>(p);
+    cudaDeviceSynchronize();
+    const int m0 = *miss;
     cudaEventRecord(e0);
     const int reps = 5;
     for (int r = 0; r < reps; ++r) v.k<<<B, v.threads>>>(p);
@@ -80,8 +108,11 @@ int main(int argc, char** argv) {
     ms /= reps;
     // SM-clocks per (sample, elimination step): how long one SM spends per step of one sample
     const double clk = double(ms) * 1e-3 * clk_khz * 1e3 * sms / (double(B) * N);
-    printf("%-22s %8.3f ms  %7.1f SM-clk per sample-step  (x2 CTAs/SM: %6.0f clk per CTA step)  %s\n", v.name, ms,
-           clk, 2 * clk, cudaGetErrorString(cudaGetLastError()));
-  }
+    printf("%-30s %8.3f ms  %7.1f SM-clk per sample-step  (x2 CTAs/SM: %6.0f clk per CTA step) misses %d/%d  %s\n",
+           v.name, ms, clk, 2 * clk, m0, B, cudaGetErrorString(cudaGetLastError()));
+  };
+  for (const V& v : vs) run(v);
+  add_diag<<<256, 256>>>(J, ldj, N, B, 10.0);
+  for (const V& v : vd) run(v);
   return 0;
 }
