@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
-    ap.add_argument("--cpu-sample", type=int, default=49152,
+    ap.add_argument("--cpu-sample", type=int, default=65536,
                     help="μ samples in the cpu_baseline leg (≈10–30 s of host work at cfg 2)")
     ap.add_argument("--ref-sample", type=int, default=16384,
                     help="μ samples per step of --impl reference (bounded so the run ends in minutes)")

@@ -290,3 +290,25 @@ def test_concurrent_streams(cfg_model, dms):
         b = dm.solve(mu[256:], stream=s2)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([a.u, b.u]), ref_u)
+
+
+@pytest.mark.parametrize("n", [40, 100])
+def test_pivot_hint_misses_take_the_exact_path(n):
+    """Rows of A₀ permuted: partial pivoting picks a non-identity order, so the speculative kernel's identity hint
+    fails at the first Newton iteration and every sample is re-run by the exact full-search kernel; from the
+    second iteration the hint (the previous order) holds.  Results must equal the oracle's either way."""
+    rng = np.random.default_rng(n)
+    base = synthetic.make_model(n, 3, "trig3", seed=n)
+    perm = rng.permutation(n)
+    A = base.A.copy()
+    A[0] = A[0][perm] * 3.0 + 0.0                       # row-permuted dominant term
+    model = ReducedModel(A=A, C=base.C, f=base.f, theta=base.theta)
+    mu = synthetic.make_mu(256, 50.0, seed=n)
+    with online.DeviceModel(model, 0) as dm:
+        u, _, it, st, _, stats = device_solve(dm, mu)
+    ur, itr, str_, _ = oracle.solve_batch(model, mu)
+    assert np.array_equal(st, str_) and np.all(st == 0)
+    assert rel_err(u, ur) <= REL
+    check_counts(model, mu, it, itr)
+    assert stats["pivot_fallbacks"] >= len(mu)           # at least the first iteration of every sample
+    assert stats["pivot_fallbacks"] < stats["sample_iterations"]
