@@ -2,6 +2,7 @@
 // (rbns_newton.cuh); kept in its own translation unit so the instantiations compile in parallel with the rest
 // of the library.  A few fixed shapes cover every N ≤ 127 (RS·TGR ≥ N rows, CS·TGC ≥ N+1 columns).
 #include "rbns_launch.h"
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -158,7 +159,13 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
     NewtonParams q = p;
     q.sub = p.miss_list;
     q.n_sub = p.miss_count;
-    s->exact<<<p.n, s->tgr * s->tgc, 0, st>>>(q);
+    static const int sms = [] {
+      int dev = 0, v = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
+    }();
+    s->exact<<<std::min(p.n, 2 * sms), s->tgr * s->tgc, 0, st>>>(q);
     *launches = 2;
   } else {
     s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);

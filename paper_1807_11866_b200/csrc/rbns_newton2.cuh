@@ -279,17 +279,23 @@ template <int TGR, int TGC, int RS, int CS, int MODE = 0>
 __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_gj2_kernel(const NewtonParams p) {
   static_assert(RS <= 32 && TGR <= 32 && TGC <= 32 && (TGR * TGC) % 32 == 0, "shape");
   __shared__ GJ2Shared<TGR, TGC, RS, CS> sh;
-  const int i_s = newton_position(p);
-  if (i_s < 0) return;
-  const int b = p.act[i_s];
+  // one sample per CTA, or (subset launch: the samples a speculative pass handed back, device-side count) a
+  // grid-stride loop over the subset so the launch can be small
+  const int n = p.sub ? *p.n_sub : p.n;
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
-  double a[RS][CS];
-  gj_load_system<TGR, TGC, RS, CS>(p, i_s, b, a, sh);
-  bool sing = false;
-  gj2_block<TGR, TGC, RS, CS, 0, MODE>(a, sing, p.N, tr, tc, sh);
-  gj_finish<TGR, TGC, RS, CS>(p, b, a, sing, sh);
-  if (p.hint_out && !sing) {  // the order partial pivoting chose: the next iteration's speculation hint
-    for (int i = tid; i < p.N; i += TGR * TGC) p.hint_out[int64_t(b) * p.N + i] = int16_t(sh.perm[i]);
+#pragma unroll 1
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const int i_s = p.sub ? p.sub[j] : j;
+    const int b = p.act[i_s];
+    double a[RS][CS];
+    gj_load_system<TGR, TGC, RS, CS>(p, i_s, b, a, sh);
+    bool sing = false;
+    gj2_block<TGR, TGC, RS, CS, 0, MODE>(a, sing, p.N, tr, tc, sh);
+    gj_finish<TGR, TGC, RS, CS>(p, b, a, sing, sh);
+    if (p.hint_out && !sing) {  // the order partial pivoting chose: the next iteration's speculation hint
+      for (int i = tid; i < p.N; i += TGR * TGC) p.hint_out[int64_t(b) * p.N + i] = int16_t(sh.perm[i]);
+    }
+    __syncthreads();  // shared memory is reused by the next sample
   }
 }
 

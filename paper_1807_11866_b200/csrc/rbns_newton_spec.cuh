@@ -142,8 +142,8 @@ __device__ __forceinline__ bool gjs_block(double (&a)[RS][CS], unsigned& pmask, 
   }
 }
 
-template <int TGR, int TGC, int RS, int CS>
-__global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_gjs_kernel(const NewtonParams p) {
+template <int TGR, int TGC, int RS, int CS, int MINB = (TGR * TGC <= 128 ? 2 : 1)>
+__global__ void __launch_bounds__(TGR * TGC, MINB) newton_gjs_kernel(const NewtonParams p) {
   using SH = GJSShared<TGR, TGC, RS, CS>;
   static_assert(RS <= 32 && TGR <= 32 && TGC <= 32 && (TGR * TGC) % 32 == 0, "shape");
   constexpr int NT = TGR * TGC, NR = TGR * RS;

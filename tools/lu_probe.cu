@@ -79,6 +79,7 @@ int main(int argc, char** argv) {
       {"gjs (dominant J: hint hits)", newton_gjs_kernel<8, 16, 13, 7>, 128},
       {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
       {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
+      {"gjs wide 16x16 2CTA/SM", newton_gjs_kernel<16, 16, 7, 7, 2>, 256},
       {"gj1 wide 16x16 (dominant J)", newton_gj_kernel<16, 16, 7, 7>, 256},
   };
   cudaEvent_t e0, e1;
