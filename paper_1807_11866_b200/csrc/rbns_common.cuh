@@ -117,7 +117,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // FP64 tensor-core MMA (lowers to DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) * B(4x8).
 // Thread (g = lane>>2, t = lane&3) supplies A[g][t], B[t][g]; holds D[g][2t], D[g][2t+1].
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }

@@ -53,12 +53,6 @@ struct ContractParams {
 #ifndef RBNS_BN
 #define RBNS_BN 128
 #endif
-#ifndef RBNS_CONTRACT_SCALE_A
-#define RBNS_CONTRACT_SCALE_A 0
-#endif
-#ifndef RBNS_CONTRACT_MINB
-#define RBNS_CONTRACT_MINB 1
-#endif
 constexpr int kBM = 64, kBN = RBNS_BN, kWM = 2, kWN = 4;
 constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 
@@ -70,13 +64,13 @@ __host__ inline size_t contract_smem_bytes(int stages, int ldu, int qb, int ql) 
          size_t(qb + ql) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
 }
 
-#ifdef RBNS_CONTRACT_MAXNREG
-#define RBNS_CONTRACT_BOUNDS(T) __maxnreg__(RBNS_CONTRACT_MAXNREG)
-#else
-#define RBNS_CONTRACT_BOUNDS(T) __launch_bounds__(T, RBNS_CONTRACT_MINB)
-#endif
-template <int BM, int BN, int WM, int WN>
-__global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
+// SCALE_A = 0 (default): θ applied once per term to a second accumulator set (168 registers, one CTA per SM).
+// SCALE_A = 1: θ applied to the A fragments, one accumulator set (fewer registers; with MINB = 2 ≤ 112, room
+// for a co-resident Newton-update CTA).  Measured: a contraction/Newton overlap on two streams with that
+// variant ran 273 ms per cfg-2 step against 217 ms sequential (both kernels dilate: the DMMAs and the Newton
+// DFMAs share the FP64 datapath), so the library runs the default variant, one kernel at a time.
+template <int BM, int BN, int WM, int WN, int SCALE_A = 0, int MINB = 1>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     contract_kernel(const __grid_constant__ CUtensorMap tmap, const ContractParams p) {
   constexpr int NCW = WM * WN;
   constexpr int TM = BM / WM, TN = BN / WN;
@@ -162,13 +156,13 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
   uint32_t phase = 0;
 
   for (int rt = rt_begin; rt < rt_end; ++rt) {
-#if RBNS_CONTRACT_SCALE_A
-    // θ applied to the A fragments (one DMUL per fragment): a single accumulator set, fewer registers
     double acc[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    if constexpr (SCALE_A) {
+    // θ applied to the A fragments (one DMUL per fragment): a single accumulator set, fewer registers
     int q = 0, k0 = 0;
     double thq[MI];
 #pragma unroll
@@ -213,12 +207,12 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
         phase ^= 1u;
       }
     }
-#else
-    double acc[MI][NI][2], accq[MI][NI][2];
+    } else {
+    double accq[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < NI; ++ni) accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
 
     int q = 0, k0 = 0;  // current term and k offset of the sub-step (uniform over the warp)
     for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
@@ -275,7 +269,7 @@ __global__ void RBNS_CONTRACT_BOUNDS((WM * WN + 1) * 32)
         phase ^= 1u;
       }
     }
-#endif
+    }
     // epilogue: fragment (sample g, rows 2t..2t+1) -> out[sample][row] as 16-byte stores
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {

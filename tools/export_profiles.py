@@ -46,6 +46,10 @@ def main():
             shutil.copy(OUT / src, PROF / f"{tag}_{dst}")
     if (OUT / "launches.csv").exists():
         (PROF / f"{tag}_launch_summary.txt").write_text(launch_summary(OUT / "launches.csv"))
+    rep_lu = OUT / "full_lu.ncu-rep"
+    if rep_lu.exists():
+        (PROF / f"{tag}_ncu_full_lu_details.csv").write_text(ncu_csv(rep_lu, "details"))
+        (PROF / f"{tag}_ncu_full_lu_raw.csv").write_text(ncu_csv(rep_lu, "raw"))
     rep = OUT / "full.ncu-rep"
     if rep.exists():
         (PROF / f"{tag}_ncu_full_details.csv").write_text(ncu_csv(rep, "details"))
