@@ -267,6 +267,25 @@ struct Timer {
   }
 };
 
+// Per-call workspace: stream-ordered allocations and events, released on every exit path.
+struct SolveWorkspace {
+  cudaStream_t st;
+  std::vector<void*> bufs;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  explicit SolveWorkspace(cudaStream_t s) : st(s) {}
+  template <class T>
+  cudaError_t alloc(T** p, size_t bytes) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+    if (e == cudaSuccess) bufs.push_back(*p);
+    return e;
+  }
+  ~SolveWorkspace() {
+    for (void* b : bufs) cudaFreeAsync(b, st);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+  }
+};
+
 int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double* p, int8_t* status, cudaStream_t st,
             rbns_stats& stats) {
   if (!m->Np) return fail(RBNS_ERR_NO_PRESSURE, "model has no pressure-recovery operators");
@@ -274,7 +293,8 @@ int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double*
   const int64_t budget = env_int64("RBNS_RBUF_BYTES", int64_t(1) << 30);
   const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldr * 8)));
   double* rbuf = nullptr;
-  RBNS_CUDA(cudaMallocAsync(&rbuf, size_t(cap) * ldr * sizeof(double), st));
+  SolveWorkspace ws(st);
+  RBNS_CUDA(ws.alloc(&rbuf, size_t(cap) * ldr * sizeof(double)));
   const int cp = (m->Np + 31) / 32;
   int rc = RBNS_OK;
   for (int64_t c0 = 0; c0 < B && rc == RBNS_OK; c0 += cap) {
@@ -301,7 +321,6 @@ int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double*
     stats.kernel_launches += 1;
     if (cudaGetLastError() != cudaSuccess) rc = fail(RBNS_ERR_CUDA, "pressure_trisolve launch failed");
   }
-  cudaFreeAsync(rbuf, st);
   return rc;
 }
 
@@ -309,29 +328,30 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
                  int32_t* iters, int8_t* status, double* last, cudaStream_t st) {
   rbns_stats stats{};
   Timer timer(st);
-  cudaEvent_t t0, t1;
-  cudaEventCreate(&t0);
-  cudaEventCreate(&t1);
-  cudaEventRecord(t0, st);
+  SolveWorkspace ws(st);
+  RBNS_CUDA(cudaEventCreate(&ws.t0));
+  RBNS_CUDA(cudaEventCreate(&ws.t1));
+  RBNS_CUDA(cudaEventRecord(ws.t0, st));
 
   const int64_t ldj = m->vel.row_tiles * kBN;
   int32_t *act0 = nullptr, *act1 = nullptr, *dcount = nullptr;
   int16_t* hints = nullptr;  // per-sample pivot order of the previous Newton iteration (speculation hint)
-  RBNS_CUDA(cudaMallocAsync(&act0, size_t(B) * sizeof(int32_t), st));
-  RBNS_CUDA(cudaMallocAsync(&act1, size_t(B) * sizeof(int32_t), st));
-  RBNS_CUDA(cudaMallocAsync(&dcount, 3 * sizeof(int32_t), st));  // active count, hint misses, chunk misses
-  RBNS_CUDA(cudaMallocAsync(&hints, size_t(B) * m->N * sizeof(int16_t), st));
+  RBNS_CUDA(ws.alloc(&act0, size_t(B) * sizeof(int32_t)));
+  RBNS_CUDA(ws.alloc(&act1, size_t(B) * sizeof(int32_t)));
+  RBNS_CUDA(ws.alloc(&dcount, 3 * sizeof(int32_t)));  // active count, hint misses, chunk misses
+  RBNS_CUDA(ws.alloc(&hints, size_t(B) * m->N * sizeof(int16_t)));
   RBNS_CUDA(cudaMemsetAsync(dcount, 0, 3 * sizeof(int32_t), st));
   const int64_t budget = env_int64("RBNS_JBUF_BYTES", int64_t(8) << 30);
   const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldj * 8)));
   int32_t* miss_list = nullptr;  // chunk positions whose pivot hint failed (re-run by the exact kernel)
-  RBNS_CUDA(cudaMallocAsync(&miss_list, size_t(std::max<int64_t>(1, std::min<int64_t>(B, cap))) * sizeof(int32_t), st));
+  RBNS_CUDA(ws.alloc(&miss_list, size_t(std::max<int64_t>(1, std::min<int64_t>(B, cap))) * sizeof(int32_t)));
   double* jbuf = nullptr;
-  if (max_iter > 0) RBNS_CUDA(cudaMallocAsync(&jbuf, size_t(cap) * ldj * sizeof(double), st));
-  static thread_local int32_t* hcount = nullptr;
+  if (max_iter > 0) RBNS_CUDA(ws.alloc(&jbuf, size_t(cap) * ldj * sizeof(double)));
+  static thread_local int32_t* hcount = nullptr;  // pinned, one per host thread for the process lifetime
   if (!hcount) RBNS_CUDA(cudaMallocHost(&hcount, 2 * sizeof(int32_t)));
 
   init_solve<<<grid_for(B, 256), 256, 0, st>>>(act0, status, iters, last, B);
+  RBNS_CUDA(cudaGetLastError());
   RBNS_CUDA(cudaMemsetAsync(u, 0, size_t(B) * m->N * sizeof(double), st));
   stats.kernel_launches += 1;
 
@@ -383,19 +403,13 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
       timer.end(e);
     }
   }
-  cudaEventRecord(t1, st);
+  cudaEventRecord(ws.t1, st);
   if (rc == RBNS_OK) RBNS_CUDA(cudaMemcpyAsync(hcount + 1, dcount + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(hints, st);
-  cudaFreeAsync(miss_list, st);
-  cudaFreeAsync(act0, st);
-  cudaFreeAsync(act1, st);
-  cudaFreeAsync(dcount, st);
-  if (jbuf) cudaFreeAsync(jbuf, st);
   cudaError_t se = cudaStreamSynchronize(st);
   if (rc == RBNS_OK && se != cudaSuccess) rc = fail(RBNS_ERR_CUDA, std::string("solve: ") + cudaGetErrorString(se));
   if (rc == RBNS_OK) {
     float tot = 0.f;
-    cudaEventElapsedTime(&tot, t0, t1);
+    cudaEventElapsedTime(&tot, ws.t0, ws.t1);
     stats.ms_total = tot;
     stats.ms_gemm = timer.total(0);
     stats.ms_lu = timer.total(1);
@@ -405,8 +419,6 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     std::lock_guard<std::mutex> lk(m->stats_mu);
     m->stats = stats;
   }
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   return rc;
 }
 
@@ -759,12 +771,13 @@ int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int3
   int32_t* di = nullptr;
   int8_t* ds = nullptr;
   const size_t N = m->N, np = m->Np;
-  RBNS_CUDA(cudaMallocAsync(&dmu, B * 2 * sizeof(double), st));
-  RBNS_CUDA(cudaMallocAsync(&du, B * N * sizeof(double), st));
-  if (p) RBNS_CUDA(cudaMallocAsync(&dp, B * np * sizeof(double), st));
-  RBNS_CUDA(cudaMallocAsync(&dl, B * sizeof(double), st));
-  RBNS_CUDA(cudaMallocAsync(&di, B * sizeof(int32_t), st));
-  RBNS_CUDA(cudaMallocAsync(&ds, B * sizeof(int8_t), st));
+  SolveWorkspace ws(st);
+  RBNS_CUDA(ws.alloc(&dmu, B * 2 * sizeof(double)));
+  RBNS_CUDA(ws.alloc(&du, B * N * sizeof(double)));
+  if (p) RBNS_CUDA(ws.alloc(&dp, B * np * sizeof(double)));
+  RBNS_CUDA(ws.alloc(&dl, B * sizeof(double)));
+  RBNS_CUDA(ws.alloc(&di, B * sizeof(int32_t)));
+  RBNS_CUDA(ws.alloc(&ds, B * sizeof(int8_t)));
   RBNS_CUDA(cudaMemcpyAsync(dmu, mu, B * 2 * sizeof(double), cudaMemcpyHostToDevice, st));
   rc = solve_device(m, dmu, B, tol, max_iter, du, dp, di, ds, dl, st);
   if (rc == RBNS_OK) {
@@ -774,9 +787,6 @@ int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int3
     RBNS_CUDA(cudaMemcpyAsync(status, ds, B * sizeof(int8_t), cudaMemcpyDeviceToHost, st));
     RBNS_CUDA(cudaMemcpyAsync(last, dl, B * sizeof(double), cudaMemcpyDeviceToHost, st));
   }
-  for (void* ptr : {static_cast<void*>(dmu), static_cast<void*>(du), static_cast<void*>(dp), static_cast<void*>(dl),
-                    static_cast<void*>(di), static_cast<void*>(ds)})
-    if (ptr) cudaFreeAsync(ptr, st);
   cudaError_t se = cudaStreamSynchronize(st);
   if (rc == RBNS_OK && se != cudaSuccess) rc = fail(RBNS_ERR_CUDA, std::string("solve_host: ") + cudaGetErrorString(se));
   return rc;
@@ -791,7 +801,8 @@ int rbns_reduced_operator(rbns_model* m, const double* mu, const double* eta, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t ldy = m->vel.row_tiles * kBN;
   double* y = nullptr;
-  RBNS_CUDA(cudaMallocAsync(&y, size_t(B) * ldy * sizeof(double), st));
+  SolveWorkspace ws(st);
+  RBNS_CUDA(ws.alloc(&y, size_t(B) * ldy * sizeof(double)));
   int rc = launch_contract(m, m->vel, nullptr, int(B), eta, mu, y, ldy, st);
   if (rc == RBNS_OK) {
     NewtonParams np = newton_params(m);
@@ -800,7 +811,6 @@ int rbns_reduced_operator(rbns_model* m, const double* mu, const double* eta, in
     operator_readout<<<int(B), 128, 0, st>>>(y, ldy, eta, np, residual, jacobian);
     if (cudaGetLastError() != cudaSuccess) rc = fail(RBNS_ERR_CUDA, "operator_readout launch failed");
   }
-  cudaFreeAsync(y, st);
   cudaError_t se = cudaStreamSynchronize(st);
   if (rc == RBNS_OK && se != cudaSuccess) rc = fail(RBNS_ERR_CUDA, std::string("reduced_operator: ") + cudaGetErrorString(se));
   return rc;

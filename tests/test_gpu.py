@@ -317,9 +317,10 @@ def test_pivot_hint_misses_take_the_exact_path(n):
         assert stats["pivot_fallbacks"] < stats["sample_iterations"]
 
 
-@pytest.mark.parametrize("variant", ["gj1", "gj2", "gj3", "bgj"])
+@pytest.mark.parametrize("variant", ["gj1", "gj2", "gj3", "bgj", "chunks"])
 def test_alternate_newton_kernels(variant):
-    """The non-default Newton-update kernels (RBNS_NEWTON, read once per process) stay parity-green."""
+    """The non-default Newton-update kernels (RBNS_NEWTON, read once per process) stay parity-green; "chunks"
+    runs the default kernels with a 40 MB Jacobian buffer, so every Newton round is split into many chunks."""
     import os
     import subprocess
     import sys
@@ -337,7 +338,7 @@ def test_alternate_newton_kernels(variant):
         "    assert np.abs(u - ur).max() <= 1e-10 * np.abs(ur).max(), c\n"
         "    assert (it != itr).sum() <= 1 and np.all(r.status.cpu().numpy() == 0), c\n"
         "print('ok')\n")
-    env = dict(os.environ, RBNS_NEWTON=variant)
+    env = dict(os.environ, RBNS_JBUF_BYTES="40000000") if variant == "chunks" else dict(os.environ, RBNS_NEWTON=variant)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
