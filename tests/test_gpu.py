@@ -292,7 +292,7 @@ def test_concurrent_streams(cfg_model, dms):
     assert torch.equal(torch.cat([a.u, b.u]), ref_u)
 
 
-@pytest.mark.parametrize("n", [40, 100])
+@pytest.mark.parametrize("n", [40, 100, 150])
 def test_pivot_hint_misses_take_the_exact_path(n):
     """Rows of A₀ permuted: partial pivoting picks a non-identity order, so the speculative kernel's identity hint
     fails at the first Newton iteration and every sample is re-run by the exact full-search kernel; from the
@@ -303,7 +303,7 @@ def test_pivot_hint_misses_take_the_exact_path(n):
     A = base.A.copy()
     A[0] = A[0][perm] * 3.0 + 0.0                       # row-permuted dominant term
     model = ReducedModel(A=A, C=base.C, f=base.f, theta=base.theta)
-    mu = synthetic.make_mu(256, 50.0, seed=n)
+    mu = synthetic.make_mu(256 if n <= 127 else 48, 50.0, seed=n)
     with online.DeviceModel(model, 0) as dm:
         u, _, it, st, _, stats = device_solve(dm, mu)
     ur, itr, str_, _ = oracle.solve_batch(model, mu)
