@@ -244,10 +244,10 @@ def _random_model(n, q, seed):
     return ReducedModel(A=np.stack(A), C=C, f=rng.standard_normal((q, n)), theta=terms)
 
 
-@pytest.mark.parametrize("n,q", [(7, 1), (13, 3), (33, 5), (64, 16), (127, 2)])
+@pytest.mark.parametrize("n,q", [(1, 1), (7, 1), (13, 3), (33, 5), (64, 16), (127, 2), (128, 2), (207, 1)])
 def test_odd_and_extreme_shapes(n, q):
     model = _random_model(n, q, seed=n)
-    mu = synthetic.make_mu(40, 100.0, seed=n)
+    mu = synthetic.make_mu(40 if n <= 127 else 12, 100.0, seed=n)
     with online.DeviceModel(model, 0) as dm:
         u, _, it, st, _, _ = device_solve(dm, mu)
     ur, itr, str_, _ = oracle.solve_batch(model, mu)
@@ -342,3 +342,13 @@ def test_alternate_newton_kernels(variant):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+
+def test_unsupported_size_fails_loudly():
+    """N beyond the register/cluster Newton kernels (207) is rejected at model creation, not computed wrong."""
+    n = 208
+    model = ReducedModel(A=np.eye(n)[None], C=np.zeros((1, n, n, n)), f=np.ones((1, n)),
+                         theta=[affine.ThetaTerm(affine.CONST)])
+    with pytest.raises(NativeError, match="exceeds"):
+        online.DeviceModel(model, 0)

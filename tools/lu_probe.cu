@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <vector>
 
+#include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
 #include "rbns_newton2.cuh"
 #include "rbns_newton3.cuh"
@@ -77,6 +78,8 @@ int main(int argc, char** argv) {
   const V vd[] = {
       {"gj2 (dominant J)", newton_gj2_kernel<8, 16, 13, 7, 0>, 128},
       {"gjs (dominant J: hint hits)", newton_gjs_kernel<8, 16, 13, 7>, 128},
+      {"bgj 13x13x8 (dominant J)", newton_bgj_kernel<13, 13, 8>, 256},
+      {"bgj 13x14x4 (dominant J)", newton_bgj_kernel<13, 14, 4>, 128},
       {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
       {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
       {"gjs wide 16x16 2CTA/SM", newton_gjs_kernel<16, 16, 7, 7, 2>, 256},
@@ -93,15 +96,22 @@ int main(int argc, char** argv) {
   cudaMallocManaged(&mcount, sizeof(int32_t));
   p.miss_list = mlist;
   p.miss_count = mcount;
+  cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(BGJShared<13, 13, 8>)));
+  cudaFuncSetAttribute(newton_bgj_kernel<13, 14, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(BGJShared<13, 14, 4>)));
   auto run = [&](const V& v) {
+    const size_t dyn = v.k == newton_bgj_kernel<13, 13, 8>   ? sizeof(BGJShared<13, 13, 8>)
+                       : v.k == newton_bgj_kernel<13, 14, 4> ? sizeof(BGJShared<13, 14, 4>)
+                                                            : 0;
     *miss = 0;
     *mcount = 0;
-    v.k<<<B, v.threads>>>(p);
+    v.k<<<B, v.threads, dyn>>>(p);
     cudaDeviceSynchronize();
     const int m0 = *miss;
     cudaEventRecord(e0);
     const int reps = 5;
-    for (int r = 0; r < reps; ++r) v.k<<<B, v.threads>>>(p);
+    for (int r = 0; r < reps; ++r) v.k<<<B, v.threads, dyn>>>(p);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
