@@ -99,7 +99,17 @@ def cpu_baseline(cfg, model, mu, sample):
         blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
     except Exception:  # pragma: no cover
         blas = []
+    from threadpoolctl import threadpool_limits
+
+    ns = min(16, sample)
+    with threadpool_limits(1):
+        t1 = time.perf_counter()
+        for b in range(ns):
+            oracle.solve_sample(model, mu[b], tol=cfg.tol, max_iter=cfg.max_iter)
+        one = ns / (time.perf_counter() - t1)
     return {"value": sample / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "port",
+            "per_sample_1thread": {"value": one, "unit": UNIT, "sample": f"{ns} mu, oracle.solve_sample (literal "
+                                   "per-sample SPEC path: einsum on C, LAPACK LU), BLAS 1 thread"},
             "sample": f"{sample} mu of cfg{cfg.index} (first {sample} of the seeded stream), batched numpy/BLAS "
                       f"oracle (oracle/rbns_oracle.py:solve_batch, {CPU_CHUNK} mu per call on a thread pool of all cores, "
                       f"BLAS 1 thread per call), {dt:.2f} s; BLAS: {', '.join(blas)}"}
@@ -316,6 +326,16 @@ def run_ours(args, cfg, world, rank, local):
                 "flops_rule": "2*Q*N^3 per sample-iteration with u != 0 (SURVEY.md §8(d)); first Newton step "
                               "has u = 0 and runs no contraction",
                 "gemm_share_of_step": float(np.sum(gemm_ms) / np.sum(step_ms))}
+        # whole-step FP64 roofline with the full per-iteration flop count: contraction
+        # 2QN³ (u ≠ 0 only), linear assembly 2QN², loads 2QN, LU (2/3)N³, residual + solves 6N²
+        n3, n2 = cfg.n ** 3, cfg.n ** 2
+        sample_its = int(st["sample_iterations"])
+        flops_step = (contraction_its / max(args.steps, 1)) * 2.0 * cfg.q * n3 + sample_its * (
+            2.0 * cfg.q * n2 + 2.0 * cfg.q * cfg.n + (2.0 / 3.0) * n3 + 6.0 * n2)
+        e2e_tf = flops_step / (mean_ms * 1e-3) / 1e12
+        roof_e2e = {"achieved": e2e_tf, "peak": peak["tflops"], "unit": "TFLOP/s", "frac": e2e_tf / peak["tflops"],
+                    "flops_per_step": flops_step,
+                    "rule": "Σ_b iters_b·F_iter, F_iter = 2QN³[u≠0] + 2QN² + 2QN + (2/3)N³ + 6N² (SURVEY.md §8(d))"}
         line = {"metric": METRIC, "value": batch * world / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -323,7 +343,7 @@ def run_ours(args, cfg, world, rank, local):
                 "e2e": {"value": batch * world / (float(te.item()) * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "path": "rbns_solve_host (C-ABI), pinned host buffers"},
-                "roofline": roof, "gpu_launches": launches, "clocks": clocks.summary(),
+                "roofline": roof, "roofline_e2e": roof_e2e, "gpu_launches": launches, "clocks": clocks.summary(),
                 "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
                            "converged": int((res.status == 0).sum().item()), "batch": batch}}
         if not args.no_cpu_baseline:

@@ -80,6 +80,7 @@ int main(int argc, char** argv) {
       {"gjs (dominant J: hint hits)", newton_gjs_kernel<8, 16, 13, 7>, 128},
       {"bgj 13x13x8 (dominant J)", newton_bgj_kernel<13, 13, 8>, 256},
       {"bgj 13x14x4 (dominant J)", newton_bgj_kernel<13, 14, 4>, 128},
+      {"bgj 13x13x13 (dominant J)", newton_bgj_kernel<13, 13, 13>, 416},
       {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
       {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
       {"gjs wide 16x16 2CTA/SM", newton_gjs_kernel<16, 16, 7, 7, 2>, 256},
@@ -100,9 +101,12 @@ int main(int argc, char** argv) {
                        int(sizeof(BGJShared<13, 13, 8>)));
   cudaFuncSetAttribute(newton_bgj_kernel<13, 14, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(BGJShared<13, 14, 4>)));
+  cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 13>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(BGJShared<13, 13, 13>)));
   auto run = [&](const V& v) {
     const size_t dyn = v.k == newton_bgj_kernel<13, 13, 8>   ? sizeof(BGJShared<13, 13, 8>)
                        : v.k == newton_bgj_kernel<13, 14, 4> ? sizeof(BGJShared<13, 14, 4>)
+                       : v.k == newton_bgj_kernel<13, 13, 13> ? sizeof(BGJShared<13, 13, 13>)
                                                             : 0;
     *miss = 0;
     *mcount = 0;
