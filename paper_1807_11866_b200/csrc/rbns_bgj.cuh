@@ -299,10 +299,10 @@ __device__ __forceinline__ void bgj_factor_pivot(int P, int buf, int N, BGJShare
 }
 
 // Apply panel P (buffer buf) to this warp's owned column tiles selected by `mask` (bit jj).
-template <int RT, int CT, int NW>
-__device__ __forceinline__ void bgj_update(double (&acc)[(CT + NW - 1) / NW][RT][2], unsigned mask, int buf, int P,
-                                           bool spec, BGJShared<RT, CT, NW>& sh) {
-  constexpr int JJ = (CT + NW - 1) / NW;
+template <int RT, int CT, int NW, int J0>
+__device__ __forceinline__ void bgj_update(double (&acc)[(CT - J0 + NW - 1) / NW][RT][2], unsigned mask, int buf,
+                                           int P, bool spec, BGJShared<RT, CT, NW>& sh) {
+  constexpr int JJ = (CT - J0 + NW - 1) / NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (!mask) return;
   const int nc = sh.nc[buf];
@@ -357,13 +357,13 @@ __device__ __forceinline__ void bgj_update(double (&acc)[(CT + NW - 1) / NW][RT]
   }
 }
 
-template <int RT, int CT, int NW>
-__device__ __forceinline__ void bgj_copy_panel(const double (&acc)[(CT + NW - 1) / NW][RT][2], int jsel,
+template <int RT, int CT, int NW, int J0>
+__device__ __forceinline__ void bgj_copy_panel(const double (&acc)[(CT - J0 + NW - 1) / NW][RT][2], int jsel,
                                                BGJShared<RT, CT, NW>& sh) {
   constexpr int PS = BGJShared<RT, CT, NW>::PS;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int jj = 0; jj < (CT + NW - 1) / NW; ++jj) {
+  for (int jj = 0; jj < (CT - J0 + NW - 1) / NW; ++jj) {
     if (jj != jsel) continue;
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
@@ -375,10 +375,14 @@ __device__ __forceinline__ void bgj_copy_panel(const double (&acc)[(CT + NW - 1)
 }
 
 // One elimination pass: reset the shared state, load [J | −R] into the tiles, blocked Gauss–Jordan.
-template <int RT, int CT, int NW>
+// J0 = 1: column tile 0 is never held in registers — it is only ever panel 0, loaded straight into the panel
+// buffer (its columns are eliminated by their own factorization) — so 4 warps hold the 12 remaining tiles of a
+// 13-tile (N ≤ 103) system 3 apiece: balanced registers, two CTAs per SM.
+template <int RT, int CT, int NW, int J0>
 __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec,
-                                         double (&acc)[(CT + NW - 1) / NW][RT][2], BGJShared<RT, CT, NW>& sh) {
-  constexpr int JJ = (CT + NW - 1) / NW;
+                                         double (&acc)[(CT - J0 + NW - 1) / NW][RT][2], BGJShared<RT, CT, NW>& sh) {
+  constexpr int JJ = (CT - J0 + NW - 1) / NW;
+  constexpr int PS = BGJShared<RT, CT, NW>::PS;
   constexpr int NR = 8 * RT;
   constexpr int NT = NW * 32;
   constexpr int NB = BGJShared<RT, CT, NW>::NB;
@@ -400,7 +404,7 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
   // ---- load the owned tiles of J ----
 #pragma unroll
   for (int jj = 0; jj < JJ; ++jj) {
-    const int j = warp + NW * jj;
+    const int j = J0 + warp + NW * jj;
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
       const int r = 8 * i + g;
@@ -413,6 +417,12 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
       }
     }
   }
+  if constexpr (J0 == 1) {  // column tile 0 goes straight to the panel buffer
+    for (int e = tid; e < NR * 8; e += NT) {
+      const int r = e >> 3, c = e & 7;
+      sh.panel[r * PS + c] = (r < N && c < N) ? __ldcs(&Jb[int64_t(r) * N + c]) : 0.0;
+    }
+  }
   if (warp == 0) RBNS_TR(spec ? 1 : 101);
 
   // ---- right-hand side −R = f − ½ J u − ½ L(μ)u as column N ----
@@ -422,7 +432,7 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
     for (int i = 0; i < RT; ++i) part[i] = 0.0;
 #pragma unroll
     for (int jj = 0; jj < JJ; ++jj) {
-      const int c0 = 8 * (warp + NW * jj) + 2 * t;
+      const int c0 = 8 * (J0 + warp + NW * jj) + 2 * t;
       const double u0 = c0 < N ? p.u[int64_t(b) * N + c0] : 0.0;
       const double u1 = c0 + 1 < N ? p.u[int64_t(b) * N + c0 + 1] : 0.0;
 #pragma unroll
@@ -441,16 +451,21 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
         double ju = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) ju += sh.rowred[w][r];
+        if constexpr (J0 == 1) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c < N) ju = fma(sh.panel[r * PS + c], p.u[int64_t(b) * N + c], ju);
+        }
         rhs = newton_rhs(p, Jb, r, ju, sh.w);
       }
       sh.rhs[r] = rhs;
     }
     __syncthreads();
     const int jr = N / 8;
-    if (warp == jr % NW && t == (N % 8) / 2) {
+    if (jr >= J0 && warp == (jr - J0) % NW && t == (N % 8) / 2) {
 #pragma unroll
       for (int jj = 0; jj < JJ; ++jj)
-        if (warp + NW * jj == jr) {
+        if (J0 + warp + NW * jj == jr) {
 #pragma unroll
           for (int i = 0; i < RT; ++i) {
             if (N & 1)
@@ -471,25 +486,27 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
     unsigned m = 0;
 #pragma unroll
     for (int jj = 0; jj < JJ; ++jj)
-      if (warp + NW * jj > q && warp + NW * jj < CT) m |= 1u << jj;
+      if (J0 + warp + NW * jj > q && J0 + warp + NW * jj < CT) m |= 1u << jj;
     return m;
   };
 #pragma unroll 1
   for (int P = -1; P < NP; ++P) {
     if (sh.sing || sh.fail) break;
     const int nxt = P + 1;
-    const bool owner = nxt < NP && warp == nxt % NW;
+    const bool owner = nxt < NP && (nxt < J0 ? warp == 0 : warp == (nxt - J0) % NW);
     // The owner shares its SM sub-partition (warp id mod 4) with one partner warp when NW == 8; DMMAs and
     // FP64 FMAs share that sub-partition's datapath, so the partner finishes its DMMA updates first and the
     // factorization then runs without competing tensor-core traffic (pair barrier, 64 threads).
     const int o = nxt % NW;
-    const bool partner = NW == 8 && nxt < NP && warp == (o + 4) % NW;
+    const bool partner = J0 == 0 && NW == 8 && nxt < NP && warp == (o + 4) % NW;
     if (owner) {
-      const int jn = nxt / NW;
+      const int jn = (nxt - J0) / NW;
       if (warp == 0) RBNS_TR(8 + 4 * nxt);
-      if (P >= 0) bgj_update<RT, CT, NW>(acc, 1u << jn, P % NB, P, spec, sh);
-      bgj_copy_panel<RT, CT, NW>(acc, jn, sh);
-      if (NW == 8) asm volatile("bar.sync %0, 64;" ::"r"(1 + (o & 3)) : "memory");
+      if (nxt >= J0) {  // (J0 = 1: panel 0 is already in the panel buffer)
+        if (P >= 0) bgj_update<RT, CT, NW, J0>(acc, 1u << jn, P % NB, P, spec, sh);
+        bgj_copy_panel<RT, CT, NW, J0>(acc, jn, sh);
+      }
+      if (J0 == 0 && NW == 8) asm volatile("bar.sync %0, 64;" ::"r"(1 + (o & 3)) : "memory");
       if (warp == 0) RBNS_TR(9 + 4 * nxt);
       if (spec)
         bgj_factor_spec<RT, CT, NW>(nxt, nxt % NB, N, sh);
@@ -499,21 +516,22 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
       if (P >= 0) pend = P;
     } else {
       if (pend >= 0) {
-        bgj_update<RT, CT, NW>(acc, tiles_above(pend + 1), pend % NB, pend, spec, sh);
+        bgj_update<RT, CT, NW, J0>(acc, tiles_above(pend + 1), pend % NB, pend, spec, sh);
         pend = -1;
       }
-      if (P >= 0) bgj_update<RT, CT, NW>(acc, tiles_above(P), P % NB, P, spec, sh);
+      if (P >= 0) bgj_update<RT, CT, NW, J0>(acc, tiles_above(P), P % NB, P, spec, sh);
       if (partner) asm volatile("bar.sync %0, 64;" ::"r"(1 + (o & 3)) : "memory");
     }
     __syncthreads();
     if (warp == 0) RBNS_TR(11 + 4 * nxt);
   }
-  if (pend >= 0 && !sh.sing && !sh.fail) bgj_update<RT, CT, NW>(acc, tiles_above(pend + 1), pend % NB, pend, spec, sh);
+  if (pend >= 0 && !sh.sing && !sh.fail)
+    bgj_update<RT, CT, NW, J0>(acc, tiles_above(pend + 1), pend % NB, pend, spec, sh);
 }
 
-template <int RT, int CT, int NW>
+template <int RT, int CT, int NW, int J0 = 0>
 __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(const NewtonParams p) {
-  constexpr int JJ = (CT + NW - 1) / NW;
+  constexpr int JJ = (CT - J0 + NW - 1) / NW;
   constexpr int NT = NW * 32;
   extern __shared__ __align__(16) unsigned char bgj_smem[];  // dynamic: sizeof(BGJShared) can exceed 48 KB
   BGJShared<RT, CT, NW>& sh = *reinterpret_cast<BGJShared<RT, CT, NW>*>(bgj_smem);
@@ -530,7 +548,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   // speculative pass (partial pivoting without interchanges); on a rejected speculation, the full pivot search
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
-    bgj_pass<RT, CT, NW>(p, b, pass == 0, acc, sh);
+    bgj_pass<RT, CT, NW, J0>(p, b, pass == 0, acc, sh);
     __syncthreads();
     if (!sh.fail) break;
     __syncthreads();
@@ -541,10 +559,10 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   const bool sing = sh.sing != 0;
   if (!sing) {
     const int jr = N / 8, NP = (N + 7) / 8;
-    if (jr >= NP && warp == jr % NW && t == (N % 8) / 2) {  // RHS in its own tile (else set by the factor)
+    if (jr >= NP && jr >= J0 && warp == (jr - J0) % NW && t == (N % 8) / 2) {  // RHS in its own tile
 #pragma unroll
       for (int jj = 0; jj < JJ; ++jj)
-        if (warp + NW * jj == jr) {
+        if (J0 + warp + NW * jj == jr) {
 #pragma unroll
           for (int i = 0; i < RT; ++i) sh.rhs[8 * i + g] = (N & 1) ? acc[jj][i][1] : acc[jj][i][0];
         }

@@ -98,7 +98,8 @@ struct BShape {
 const BShape kBShapes[] = {
     RBNS_BS(2, 2, 2),     // N ≤ 15
     RBNS_BS(7, 7, 4),     // N ≤ 55
-    RBNS_BS(13, 13, 8),   // N ≤ 103
+    {13, 13, 4, newton_bgj_kernel<13, 13, 4, 1>, sizeof(BGJShared<13, 13, 4>)},  // N ≤ 103 (tile 0 never in
+                                                                                  // registers: 4 warps, 2 CTAs/SM)
     RBNS_BS(16, 16, 8),   // N ≤ 127
 };
 #undef RBNS_BS

@@ -81,6 +81,7 @@ int main(int argc, char** argv) {
       {"bgj 13x13x8 (dominant J)", newton_bgj_kernel<13, 13, 8>, 256},
       {"bgj 13x14x4 (dominant J)", newton_bgj_kernel<13, 14, 4>, 128},
       {"bgj 13x13x13 (dominant J)", newton_bgj_kernel<13, 13, 13>, 416},
+      {"bgj 13x13x4 J0=1 (dominant J)", newton_bgj_kernel<13, 13, 4, 1>, 128},
       {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
       {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
       {"gjs wide 16x16 2CTA/SM", newton_gjs_kernel<16, 16, 7, 7, 2>, 256},
@@ -103,10 +104,16 @@ int main(int argc, char** argv) {
                        int(sizeof(BGJShared<13, 14, 4>)));
   cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 13>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(BGJShared<13, 13, 13>)));
+  cudaFuncSetAttribute(newton_bgj_kernel<12, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(BGJShared<12, 12, 4>)));
+  cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(BGJShared<13, 13, 4>)));
   auto run = [&](const V& v) {
     const size_t dyn = v.k == newton_bgj_kernel<13, 13, 8>   ? sizeof(BGJShared<13, 13, 8>)
                        : v.k == newton_bgj_kernel<13, 14, 4> ? sizeof(BGJShared<13, 14, 4>)
                        : v.k == newton_bgj_kernel<13, 13, 13> ? sizeof(BGJShared<13, 13, 13>)
+                       : v.k == newton_bgj_kernel<12, 12, 4> ? sizeof(BGJShared<12, 12, 4>)
+                       : v.k == newton_bgj_kernel<13, 13, 4, 1> ? sizeof(BGJShared<13, 13, 4>)
                                                             : 0;
     *miss = 0;
     *mcount = 0;
