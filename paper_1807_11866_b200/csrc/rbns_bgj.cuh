@@ -153,8 +153,9 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
         g |= rr[s] > k && rr[s] < N && fabs(pr[s][0]) > fabs(piv);
       gt |= __ballot_sync(0xffffffffu, g);
     }
-    bad = gt != 0u;
-    if (bad || !(fabs(piv) >= 2.2250738585072014e-308) || !isfinite(piv)) break;  // warp-uniform
+    // no early exit: the flags are collected and checked once after the panel (a rejected speculation reruns
+    // the whole sample with the pivot search), so the branch never waits on the ballots inside the chain
+    bad |= gt != 0u || !(fabs(piv) >= 2.2250738585072014e-308) || !isfinite(piv);
     double l[RPL];
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {  // next column first: it carries the next pivot (critical path)
@@ -176,12 +177,7 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
   }
   if (lane == 0) {
     sh.nc[buf] = c;
-    if (c < nc) {
-      if (bad)
-        sh.fail = 1;  // partial pivoting would interchange rows: redo this sample with the pivot search
-      else
-        sh.sing = 1;
-    }
+    if (bad) sh.fail = 1;  // an interchange (or a zero / non-finite pivot): redo with the pivot search
   }
   if (N / 8 == P) {  // the right-hand side column (index N - 8P = nc in this panel) is now pr[s][0]
 #pragma unroll
