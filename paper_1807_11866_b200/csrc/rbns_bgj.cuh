@@ -541,12 +541,19 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   __syncthreads();
   double acc[JJ][RT][2];
   if (warp == 0) RBNS_TR(0);
-  // speculative pass (partial pivoting without interchanges); on a rejected speculation, the full pivot search
+  // speculative pass (partial pivoting without interchanges); on a rejected speculation, the full pivot search.
+  // A sample whose previous Newton iteration already needed interchanges (non-identity hint) goes straight to
+  // the search pass.
+  bool identity = true;
+  if (p.hint_in)
+    for (int k = tid; k < N; k += NT) identity &= p.hint_in[int64_t(b) * N + k] == k;
+  const int first_pass = __syncthreads_and(identity) ? 0 : 1;
 #pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = first_pass; pass < 2; ++pass) {
     bgj_pass<RT, CT, NW, J0>(p, b, pass == 0, acc, sh);
     __syncthreads();
     if (!sh.fail) break;
+    if (tid == 0 && p.spec_miss) atomicAdd(p.spec_miss, 1);
     __syncthreads();
   }
   if (warp == 0) RBNS_TR(sh.fail ? 201 : 200);
@@ -602,6 +609,9 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
     p.status[b] = int8_t(st);
     p.iters[b] = p.iter;
     if (!sing && finite) p.last[b] = sqrt(d2);
+  }
+  if (p.hint_out && !sing) {  // the order used: the next Newton iteration's hint
+    for (int k = tid; k < N; k += NT) p.hint_out[int64_t(b) * N + k] = int16_t(sh.perm[k]);
   }
   if (warp == 0) RBNS_TR(202);
 }

@@ -98,6 +98,7 @@ struct BShape {
 const BShape kBShapes[] = {
     RBNS_BS(2, 2, 2),     // N ≤ 15
     RBNS_BS(7, 7, 4),     // N ≤ 55
+    RBNS_BS(12, 12, 4),   // N ≤ 95
     {13, 13, 4, newton_bgj_kernel<13, 13, 4, 1>, sizeof(BGJShared<13, 13, 4>)},  // N ≤ 103 (tile 0 never in
                                                                                   // registers: 4 warps, 2 CTAs/SM)
     RBNS_BS(16, 16, 8),   // N ≤ 127
@@ -112,12 +113,16 @@ const BShape* bplan(int N) {
 
 // RBNS_NEWTON=bgj selects the blocked DMMA kernel (rbns_bgj.cuh); the default is the rank-1 register kernel
 // (rbns_newton.cuh), currently the faster of the two at N ≤ 104 (both are parity-tested).
-bool use_blocked() {
-  static const bool blocked = [] {
+// The blocked kernel is the default where it measured faster (88 < N ≤ 103: cfg-2 Newton update 78 ms vs 89 ms
+// for the speculative rank-1 kernel); RBNS_NEWTON=bgj forces it for every N it covers, any other RBNS_NEWTON
+// value forces the rank-1 kernels.
+bool use_blocked(int N) {
+  static const int mode = [] {
     const char* v = std::getenv("RBNS_NEWTON");
-    return v && std::strcmp(v, "bgj") == 0;
+    if (!v || !*v) return 0;
+    return std::strcmp(v, "bgj") == 0 ? 1 : 2;
   }();
-  return blocked;
+  return mode == 1 || (mode == 0 && N > 88 && N <= 103);
 }
 }  // namespace
 
@@ -128,7 +133,7 @@ bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr 
 
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches) {
   *launches = 1;
-  if (use_blocked()) {
+  if (use_blocked(p.N)) {
     if (const BShape* b = bplan(p.N)) {
       static bool attr_set[sizeof(kBShapes) / sizeof(kBShapes[0])] = {};
       const int idx = int(b - kBShapes);
