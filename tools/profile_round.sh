@@ -12,5 +12,5 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 P="python tools/profile_case.py 2 65536"
 $P > gpurun_out/plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"contract_kernel" -s 2 -c 1 -o gpurun_out/full $P > gpurun_out/ncu_full.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"newton_gjs" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"newton_bgj" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
 tail -2 gpurun_out/ncu_full.log
