@@ -22,6 +22,7 @@ __global__ void fill(double* x, size_t n, unsigned seed) {
 }
 
 using K = void (*)(const NewtonParams);
+using NewtonKernel = K;
 
 __global__ void add_diag(double* J, int64_t ldj, int N, int B, double d) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(B) * N; i += int64_t(gridDim.x) * blockDim.x)
@@ -82,6 +83,7 @@ int main(int argc, char** argv) {
       {"bgj 13x14x4 (dominant J)", newton_bgj_kernel<13, 14, 4>, 128},
       {"bgj 13x13x13 (dominant J)", newton_bgj_kernel<13, 13, 13>, 416},
       {"bgj 13x13x4 J0=1 (dominant J)", newton_bgj_kernel<13, 13, 4, 1>, 128},
+      {"bgj 13x13x4 J0=1 1CTA/SM", newton_bgj_kernel<13, 13, 4, 1>, 129},
       {"gj2 wide 16x16 (dominant J)", newton_gj2_kernel<16, 16, 7, 7, 0>, 256},
       {"gjs wide 16x16 (dominant J)", newton_gjs_kernel<16, 16, 7, 7>, 256},
       {"gjs wide 16x16 2CTA/SM", newton_gjs_kernel<16, 16, 7, 7, 2>, 256},
@@ -106,10 +108,10 @@ int main(int argc, char** argv) {
                        int(sizeof(BGJShared<13, 13, 13>)));
   cudaFuncSetAttribute(newton_bgj_kernel<12, 12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(sizeof(BGJShared<12, 12, 4>)));
-  cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(sizeof(BGJShared<13, 13, 4>)));
+  cudaFuncSetAttribute(newton_bgj_kernel<13, 13, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   auto run = [&](const V& v) {
-    const size_t dyn = v.k == newton_bgj_kernel<13, 13, 8>   ? sizeof(BGJShared<13, 13, 8>)
+    const size_t dyn = v.threads == 129 ? size_t(120 * 1024)
+                       : v.k == newton_bgj_kernel<13, 13, 8>   ? sizeof(BGJShared<13, 13, 8>)
                        : v.k == newton_bgj_kernel<13, 14, 4> ? sizeof(BGJShared<13, 14, 4>)
                        : v.k == newton_bgj_kernel<13, 13, 13> ? sizeof(BGJShared<13, 13, 13>)
                        : v.k == newton_bgj_kernel<12, 12, 4> ? sizeof(BGJShared<12, 12, 4>)
@@ -117,12 +119,13 @@ int main(int argc, char** argv) {
                                                             : 0;
     *miss = 0;
     *mcount = 0;
-    v.k<<<B, v.threads, dyn>>>(p);
+    const int nthr = v.threads == 129 ? 128 : v.threads;
+    v.k<<<B, nthr, dyn>>>(p);
     cudaDeviceSynchronize();
     const int m0 = *miss;
     cudaEventRecord(e0);
     const int reps = 5;
-    for (int r = 0; r < reps; ++r) v.k<<<B, v.threads, dyn>>>(p);
+    for (int r = 0; r < reps; ++r) v.k<<<B, nthr, dyn>>>(p);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -133,6 +136,35 @@ int main(int argc, char** argv) {
     printf("%-30s %8.3f ms  %7.1f SM-clk per sample-step  (x2 CTAs/SM: %6.0f clk per CTA step) misses %d/%d  %s\n",
            v.name, ms, clk, 2 * clk, m0, B, cudaGetErrorString(cudaGetLastError()));
   };
+  if (N <= 55) {  // small systems: one-warp rank-1 kernel vs blocked kernels
+    cudaFuncSetAttribute(newton_bgj_kernel<7, 7, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(BGJShared<7, 7, 4>)));
+    cudaFuncSetAttribute(newton_bgj_kernel<7, 7, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(sizeof(BGJShared<7, 7, 3>)));
+    add_diag<<<256, 256>>>(J, ldj, N, B, 10.0);
+    const V small[] = {
+        {"gjs 4x8x13x7", newton_gjs_kernel<4, 8, 13, 7>, 32},
+        {"gj2 4x8x13x7", newton_gj2_kernel<4, 8, 13, 7, 0>, 32},
+    };
+    for (const V& v : small) run(v);
+    for (int w = 0; w < 2; ++w) {
+      const NewtonKernel k = w == 0 ? newton_bgj_kernel<7, 7, 4> : newton_bgj_kernel<7, 7, 3, 1>;
+      const size_t sm = w == 0 ? sizeof(BGJShared<7, 7, 4>) : sizeof(BGJShared<7, 7, 3>);
+      const int thr = w == 0 ? 128 : 96;
+      k<<<B, thr, sm>>>(p);
+      cudaDeviceSynchronize();
+      cudaEventRecord(e0);
+      for (int r = 0; r < 5; ++r) k<<<B, thr, sm>>>(p);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= 5;
+      printf("%-30s %8.3f ms  %7.1f SM-clk per sample-step  %s\n", w == 0 ? "bgj 7x7x4" : "bgj 7x7x3 J0=1", ms,
+             double(ms) * 1e-3 * clk_khz * 1e3 * sms / (double(B) * N), cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+  }
   for (const V& v : vs) run(v);
   add_diag<<<256, 256>>>(J, ldj, N, B, 10.0);
   for (const V& v : vd) run(v);
