@@ -203,7 +203,7 @@ NewtonParams newton_params(const rbns_model* m) {
 int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
                   const double* mu, int iter, int max_iter, double tol, int32_t* iters, int8_t* status, double* last,
                   int16_t* hints, int32_t* spec_miss, int32_t* miss_list, int32_t* miss_count, int* launches,
-                  cudaStream_t st) {
+                  bool prefer_rank1, cudaStream_t st) {
   if (n <= 0) return RBNS_OK;
   NewtonParams p = newton_params(m);
   p.act = act;
@@ -223,6 +223,7 @@ int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int
   p.spec_miss = spec_miss;
   p.miss_list = miss_list;
   p.miss_count = miss_count;
+  p.prefer_rank1 = prefer_rank1 ? 1 : 0;
   RBNS_CUDA(launch_newton_update(p, st, launches));
   return RBNS_OK;
 }
@@ -357,6 +358,11 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
 
   int rc = RBNS_OK;
   int64_t n_act = B;
+  // The blocked Newton kernel speculates the identity pivot order; once a round shows samples that need row
+  // interchanges, the remaining rounds use the rank-1 kernel, whose speculation follows each sample's own
+  // previous order (hints are written by both).
+  bool prefer_rank1 = false;
+  int32_t misses_seen = 0;
   for (int it = 1; it <= max_iter && n_act > 0 && rc == RBNS_OK; ++it) {
     const int first = it == 1;
     stats.sample_iterations += n_act;
@@ -379,7 +385,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
       const int e = timer.begin(1);
       int nl = 0;
       rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, hints,
-                         dcount + 1, miss_list, dcount + 2, &nl, st);
+                         dcount + 1, miss_list, dcount + 2, &nl, prefer_rank1, st);
       timer.end(e);
       if (rc) break;
       stats.lu_launches += nl;
@@ -389,8 +395,10 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     compact_active<<<1, kCompactThreads, 0, st>>>(act0, int32_t(n_act), status, act1, dcount);
     stats.kernel_launches += 1;
     RBNS_CUDA(cudaGetLastError());
-    RBNS_CUDA(cudaMemcpyAsync(hcount, dcount, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    RBNS_CUDA(cudaMemcpyAsync(hcount, dcount, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     RBNS_CUDA(cudaStreamSynchronize(st));
+    if (int64_t(hcount[1] - misses_seen) * 64 > n_act) prefer_rank1 = true;  // > 1/64 of the round missed
+    misses_seen = hcount[1];
     n_act = *hcount;
     std::swap(act0, act1);
   }

@@ -133,7 +133,7 @@ bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr 
 
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches) {
   *launches = 1;
-  if (use_blocked(p.N)) {
+  if (!p.prefer_rank1 && use_blocked(p.N)) {
     if (const BShape* b = bplan(p.N)) {
       static bool attr_set[sizeof(kBShapes) / sizeof(kBShapes[0])] = {};
       const int idx = int(b - kBShapes);

@@ -47,6 +47,7 @@ struct NewtonParams {
   int32_t* miss_count;         //   … and their number (device counter, zeroed per chunk)
   const int32_t* sub;          // exact kernels: run only the chunk positions sub[0 .. *n_sub) (NULL: all n)
   const int32_t* n_sub;
+  int32_t prefer_rank1;        // host policy: pivoting seen, use the hinted rank-1 kernel over the blocked one
 };
 
 // CTA → chunk position (and whether this CTA has work) for the exact kernels' optional subset launch
