@@ -53,7 +53,13 @@ struct ContractParams {
 #ifndef RBNS_BN
 #define RBNS_BN 128
 #endif
-constexpr int kBM = 64, kBN = RBNS_BN, kWM = 2, kWN = 4;
+#ifndef RBNS_WN
+#define RBNS_WN 4
+#endif
+#ifndef RBNS_SCALE_A_DEFAULT
+#define RBNS_SCALE_A_DEFAULT 0
+#endif
+constexpr int kBM = 64, kBN = RBNS_BN, kWM = 2, kWN = RBNS_WN;
 constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 
 // u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups

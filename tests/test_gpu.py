@@ -244,7 +244,8 @@ def _random_model(n, q, seed):
     return ReducedModel(A=np.stack(A), C=C, f=rng.standard_normal((q, n)), theta=terms)
 
 
-@pytest.mark.parametrize("n,q", [(1, 1), (7, 1), (13, 3), (33, 5), (64, 16), (127, 2), (128, 2), (207, 1)])
+@pytest.mark.parametrize("n,q", [(1, 1), (7, 1), (13, 3), (33, 5), (64, 16), (89, 2), (91, 3), (95, 1), (96, 2),
+                                 (103, 4), (104, 1), (127, 2), (128, 2), (207, 1)])
 def test_odd_and_extreme_shapes(n, q):
     model = _random_model(n, q, seed=n)
     mu = synthetic.make_mu(40 if n <= 127 else 12, 100.0, seed=n)
