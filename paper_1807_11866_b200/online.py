@@ -13,6 +13,7 @@ Public API (names and meaning follow the SPEC):
 * :func:`solve_block_batch` (rm, μ[B,2]) → :class:`BatchSolution` — the batch sweep API.
 * :func:`reduced_operator` (rm, μ, η) → (residual, Jacobian) — SPEC.md:500-508.
 * :func:`reconstruct_pressure` — recovery alone for given velocities (SPEC.md:523 step 2).
+* :func:`sweep_report` — the batch sweep's tabular (CSV) report.
 * :class:`DeviceModel` — the uploaded, immutable operator handle (one per device), for callers that keep
   tensors on the GPU.
 """
@@ -286,3 +287,38 @@ def reconstruct_pressure(rm: ReducedModel, mus, u, device: int = 0) -> torch.Ten
     """Pressure recovery for given velocity coefficients."""
     p, _ = device_model(rm, device).recover_pressure(mus, u)
     return p
+
+
+SWEEP_COLUMNS = ("phi", "u_inf", "solver", "iters", "status", "last_update", "converged",
+                 "t_assembly_s", "t_solve_s", "t_recovery_s")
+
+
+def sweep_report(mus, sol: BatchSolution, path=None, solver: str = "block") -> str:
+    """Tabular report of a batch sweep ("batch sweep API over parameter grids returning a tabular
+    report (CSV columns: φ, u∞, solver, iters, errors if reference available, phase timings)").  Phase timings
+    are the batch's device times divided evenly over its samples.  Deterministic text (fixed column order,
+    repr-exact floats); written to ``path`` when given, returned either way."""
+    import csv
+    import io
+
+    mus = np.asarray(mus.cpu() if isinstance(mus, torch.Tensor) else mus, dtype=np.float64).reshape(-1, 2)
+    it = sol.iters.cpu().numpy()
+    st = sol.status.cpu().numpy()
+    last = sol.last_update.cpu().numpy()
+    b = max(1, len(mus))
+    per = {k: sol.stats.get(f"ms_{k}", 0.0) * 1e-3 / b for k in ("gemm", "lu", "recovery")}
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    buf.write("# rbflow batch sweep report v1\n")
+    w.writerow(SWEEP_COLUMNS)
+    names = {CONVERGED: "CONVERGED", NON_CONVERGED: "NON_CONVERGED", SINGULAR_SYSTEM: "SINGULAR_SYSTEM",
+             SINGULAR_RECOVERY: "SINGULAR_RECOVERY", NONFINITE: "NONFINITE"}
+    for i in range(len(mus)):
+        w.writerow([repr(float(mus[i, 0])), repr(float(mus[i, 1])), solver, int(it[i]), names.get(int(st[i]), int(st[i])),
+                    repr(float(last[i])), int(st[i]) == CONVERGED, repr(per["gemm"]), repr(per["lu"]),
+                    repr(per["recovery"])])
+    text = buf.getvalue()
+    if path is not None:
+        with open(path, "w") as fh:
+            fh.write(text)
+    return text

@@ -47,3 +47,24 @@ def test_shard_bounds_partition(total, world):
         assert 0 <= s <= e <= total
         seen.extend(range(s, e))
     assert seen == list(range(total))
+
+
+def test_sweep_report_is_deterministic(tmp_path):
+    """SPEC.md:566 tabular report: fixed columns, one row per μ, byte-stable rewrite."""
+    import numpy as np
+    import torch
+
+    from paper_1807_11866_b200 import online
+
+    mus = np.array([[0.1, 20.0], [0.2, 30.0], [0.3, 40.0]])
+    sol = online.BatchSolution(u=torch.zeros(3, 4, dtype=torch.float64), p=None,
+                               iters=torch.tensor([4, 5, 20], dtype=torch.int32),
+                               status=torch.tensor([0, 0, 1], dtype=torch.int8),
+                               last_update=torch.tensor([1e-13, 2e-13, 1e-3], dtype=torch.float64),
+                               stats={"ms_gemm": 3.0, "ms_lu": 1.5, "ms_recovery": 0.0})
+    t1 = online.sweep_report(mus, sol, tmp_path / "a.csv")
+    t2 = online.sweep_report(mus, sol, tmp_path / "b.csv")
+    assert t1 == t2 == (tmp_path / "a.csv").read_text()
+    lines = t1.strip().split("\n")
+    assert lines[0].startswith("#") and lines[1].split(",") == list(online.SWEEP_COLUMNS)
+    assert len(lines) == 2 + 3 and "NON_CONVERGED" in lines[4] and lines[2].split(",")[3] == "4"
