@@ -500,6 +500,7 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
       if (warp == 0) RBNS_TR(8 + 4 * nxt);
       if (nxt >= J0) {  // (J0 = 1: panel 0 is already in the panel buffer)
         if (P >= 0) bgj_update<RT, CT, NW, J0>(acc, 1u << jn, P % NB, P, spec, sh);
+        if (warp == 0) RBNS_TR(160 + nxt);
         bgj_copy_panel<RT, CT, NW, J0>(acc, jn, sh);
       }
       if (J0 == 0 && NW == 8) asm volatile("bar.sync %0, 64;" ::"r"(1 + (o & 3)) : "memory");

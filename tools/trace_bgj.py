@@ -23,6 +23,7 @@ with online.DeviceModel(m, 0) as dm:
     for P in range(16):
         names[8 + 4 * P] = f"P{P}: lookahead-start"; names[9 + 4 * P] = f"P{P}: lookahead-done"
         names[10 + 4 * P] = f"P{P}: factor-done"; names[11 + 4 * P] = f"P{P}: barrier"
+        names[160 + P] = f"P{P}: lookahead-update-done (copy next)"
     rows = sorted((buf[i] - t0, names.get(i, str(i))) for i in range(256) if buf[i] >= t0 and buf[i] != 0)
     prev = 0
     for tt, nm in rows:
