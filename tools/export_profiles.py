@@ -62,8 +62,10 @@ def main():
                 continue
             rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
             wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
-            unit = rows[1][hdr.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rd *= units.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)  # ncu scales each metric's unit
+            wr *= units.get(rows[1][hdr.index("dram__bytes_write.sum")], 1)  # separately (Mbyte vs Gbyte)
+            scale = 1
             json.dump({"cfg2": {
                 "dram_bytes_per_launch": int((rd + wr) * scale), "dram_read_bytes": int(rd * scale),
                 "dram_write_bytes": int(wr * scale),
