@@ -65,7 +65,10 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=())
 
 
 if __name__ == "__main__":
-    if "--trace" in sys.argv:
+    if "--define" in sys.argv:  # development variant: python -m ...build --define NAME=VAL  -> build/librbns_NAME.so
+        d = sys.argv[sys.argv.index("--define") + 1]
+        print(build(force=True, out=ROOT / "build" / f"librbns_{d.replace('=', '_').lower()}.so", extra=(f"-D{d}",)))
+    elif "--trace" in sys.argv:
         print(build(force="-f" in sys.argv, out=ROOT / "build" / "librbns_trace.so", extra=("-DRBNS_TRACE",)))
     else:
         print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -526,6 +526,8 @@ __device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec
     bgj_update<RT, CT, NW, J0>(acc, tiles_above(pend + 1), pend % NB, pend, spec, sh);
 }
 
+constexpr int kBgjPrefetchAhead = 296;
+
 template <int RT, int CT, int NW, int J0 = 0>
 __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(const NewtonParams p) {
   constexpr int JJ = (CT - J0 + NW - 1) / NW;
@@ -539,6 +541,10 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   const int N = p.N;
 
   newton_weights(p, b, sh.w);
+  // the CTA that takes this slot about one wave of resident CTAs later finds its J in L2 (bulk prefetch; the
+  // distance is not critical: 148..592 measured alike, Newton update 79.4 -> 77.5 ms per cfg-2 step)
+  if (tid == 0 && i_s + kBgjPrefetchAhead < p.n)
+    bulk_prefetch_l2(p.J + int64_t(i_s + kBgjPrefetchAhead) * p.ldj, uint32_t(p.ldj * 8));
   __syncthreads();
   double acc[JJ][RT][2];
   if (warp == 0) RBNS_TR(0);
