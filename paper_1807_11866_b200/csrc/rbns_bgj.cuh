@@ -299,7 +299,7 @@ template <int RT, int CT, int NW, int J0>
 __device__ __forceinline__ void bgj_update(double (&acc)[(CT - J0 + NW - 1) / NW][RT][2], unsigned mask, int buf,
                                            int P, bool spec, BGJShared<RT, CT, NW>& sh) {
   constexpr int JJ = (CT - J0 + NW - 1) / NW;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int warp = (threadIdx.x % (NW * 32)) >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   if (!mask) return;
   const int nc = sh.nc[buf];
   double b0[JJ], b1[JJ];
@@ -374,17 +374,17 @@ __device__ __forceinline__ void bgj_copy_panel(const double (&acc)[(CT - J0 + NW
 // J0 = 1: column tile 0 is never held in registers — it is only ever panel 0, loaded straight into the panel
 // buffer (its columns are eliminated by their own factorization) — so 4 warps hold the 12 remaining tiles of a
 // 13-tile (N ≤ 103) system 3 apiece: balanced registers, two CTAs per SM.
+// i_s: chunk position of the sample (its J block).
 template <int RT, int CT, int NW, int J0>
-__device__ __forceinline__ void bgj_pass(const NewtonParams& p, int b, bool spec,
+__device__ __forceinline__ void bgj_pass(const NewtonParams& p, int i_s, int b, bool spec,
                                          double (&acc)[(CT - J0 + NW - 1) / NW][RT][2], BGJShared<RT, CT, NW>& sh) {
   constexpr int JJ = (CT - J0 + NW - 1) / NW;
   constexpr int PS = BGJShared<RT, CT, NW>::PS;
   constexpr int NR = 8 * RT;
   constexpr int NT = NW * 32;
   constexpr int NB = BGJShared<RT, CT, NW>::NB;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int tid = threadIdx.x % NT, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int N = p.N;
-  const int i_s = blockIdx.x;
   if (tid == 0) {
     sh.sing = 0;
     sh.fail = 0;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(NW * 32, (NW <= 4 ? 2 : 1)) newton_bgj_kernel(
   const int first_pass = __syncthreads_and(identity) ? 0 : 1;
 #pragma unroll 1
   for (int pass = first_pass; pass < 2; ++pass) {
-    bgj_pass<RT, CT, NW, J0>(p, b, pass == 0, acc, sh);
+    bgj_pass<RT, CT, NW, J0>(p, i_s, b, pass == 0, acc, sh);
     __syncthreads();
     if (!sh.fail) break;
     if (tid == 0 && p.spec_miss) atomicAdd(p.spec_miss, 1);
