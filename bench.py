@@ -262,7 +262,7 @@ def run_ours(args, cfg, world, rank, local):
     torch.cuda.synchronize(device)
 
     stream = torch.cuda.current_stream(device)
-    step_ms, gemm_ms, launches, contraction_its, gemm_launches = [], [], 0, 0, 0
+    step_ms, gemm_ms, lu_ms, launches, contraction_its, gemm_launches = [], [], [], 0, 0, 0
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(device)
@@ -277,6 +277,7 @@ def run_ours(args, cfg, world, rank, local):
             step_ms.append(e0.elapsed_time(e1))
             st = res.stats
             gemm_ms.append(st["ms_gemm"])
+            lu_ms.append(st["ms_lu"])
             launches += st["kernel_launches"]
             contraction_its += st["contraction_iterations"]
             gemm_launches += st["gemm_launches"]
@@ -336,6 +337,17 @@ def run_ours(args, cfg, world, rank, local):
         roof_e2e = {"achieved": e2e_tf, "peak": peak["tflops"], "unit": "TFLOP/s", "frac": e2e_tf / peak["tflops"],
                     "flops_per_step": flops_step,
                     "rule": "Σ_b iters_b·F_iter, F_iter = 2QN³[u≠0] + 2QN² + 2QN + (2/3)N³ + 6N² (SURVEY.md §8(d))"}
+        # the second kernel of the step, the batched Newton update (Gauss–Jordan with partial pivoting):
+        # N³ FMA per sample-iteration on [J | −R] as executed; LU-equivalent algorithmic count (2/3)N³ + 2N²
+        gj_flops = sample_its * 2.0 * n3
+        lu_flops = sample_its * ((2.0 / 3.0) * n3 + 2.0 * n2)
+        lu_s = float(np.mean(lu_ms)) * 1e-3
+        newton = {"kernel": "newton_bgj_kernel (blocked Gauss-Jordan, DMMA trailing updates)" if 88 < cfg.n <= 103
+                  else "Newton update kernels", "ms_per_step": lu_s * 1e3,
+                  "share_of_step": float(np.sum(lu_ms) / np.sum(step_ms)),
+                  "achieved_gj": gj_flops / lu_s / 1e12, "achieved_lu_equivalent": lu_flops / lu_s / 1e12,
+                  "peak": peak["tflops"], "unit": "TFLOP/s", "frac_gj": gj_flops / lu_s / 1e12 / peak["tflops"],
+                  "bound": "latency (per-panel factorization chain; two systems per SM fill the register file)"}
         line = {"metric": METRIC, "value": batch * world / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -343,7 +355,7 @@ def run_ours(args, cfg, world, rank, local):
                 "e2e": {"value": batch * world / (float(te.item()) * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "path": "rbns_solve_host (C-ABI), pinned host buffers"},
-                "roofline": roof, "roofline_e2e": roof_e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+                "roofline": roof, "roofline_e2e": roof_e2e, "newton_update": newton, "gpu_launches": launches, "clocks": clocks.summary(),
                 "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
                            "converged": int((res.status == 0).sum().item()), "batch": batch}}
         if not args.no_cpu_baseline:
