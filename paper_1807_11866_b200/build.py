@@ -67,7 +67,7 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=())
 if __name__ == "__main__":
     if "--define" in sys.argv:  # development variant: python -m ...build --define NAME=VAL  -> build/librbns_NAME.so
         d = sys.argv[sys.argv.index("--define") + 1]
-        print(build(force=True, out=ROOT / "build" / f"librbns_{d.replace('=', '_').lower()}.so", extra=tuple(f"-D{x}" for x in d.split(','))))
+        print(build(force=True, out=ROOT / "build" / f"librbns_{d.replace('=', '_').replace(',', '_').lower()}.so", extra=tuple(f"-D{x}" for x in d.split(','))))
     elif "--trace" in sys.argv:
         print(build(force="-f" in sys.argv, out=ROOT / "build" / "librbns_trace.so", extra=("-DRBNS_TRACE",)))
     else:

@@ -59,7 +59,10 @@ struct ContractParams {
 #ifndef RBNS_SCALE_A_DEFAULT
 #define RBNS_SCALE_A_DEFAULT 0
 #endif
-constexpr int kBM = 64, kBN = RBNS_BN, kWM = 2, kWN = RBNS_WN;
+#ifndef RBNS_WM
+#define RBNS_WM 2
+#endif
+constexpr int kBM = 64, kBN = RBNS_BN, kWM = RBNS_WM, kWN = RBNS_WN;
 constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 
 // u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups
