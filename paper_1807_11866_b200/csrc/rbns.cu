@@ -153,7 +153,8 @@ using ContractKernel = void (*)(const CUtensorMap, const ContractParams);
 constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN, RBNS_SCALE_A_DEFAULT>;
 
 int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n, const double* u, const double* mu,
-                    double* out, int64_t ldo, cudaStream_t st, bool linear_only = false) {
+                    double* out, int64_t ldo, cudaStream_t st, bool linear_only = false,
+                    const double* wts = nullptr) {
   if (n <= 0) return RBNS_OK;
   ContractParams p{};
   p.act = act;
@@ -175,6 +176,7 @@ int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n,
   p.stages = op.stages;
   p.out = out;
   p.ldo = ldo;
+  p.wts = wts;
   const int sample_tiles = (n + kBM - 1) / kBM;
   const int64_t want = 8LL * m->num_sms;
   int groups = int(std::max<int64_t>(1, (want + sample_tiles - 1) / sample_tiles));
@@ -353,6 +355,16 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
 
   init_solve<<<grid_for(B, 256), 256, 0, st>>>(act0, status, iters, last, B);
   RBNS_CUDA(cudaGetLastError());
+  // the contraction's θ weights, once per solve
+  double* wts = nullptr;
+  const int ldw = m->vel.Qb + m->vel.Ql;
+  if (max_iter > 0) {
+    RBNS_CUDA(ws.alloc(&wts, size_t(B) * ldw * sizeof(double)));
+    eval_weights<<<grid_for(B * ldw, 256), 256, 0, st>>>(mu, B, m->vel.thb, m->vel.Qb, m->vel.thl, m->vel.Ql,
+                                                        m->nu_lin, wts);
+    RBNS_CUDA(cudaGetLastError());
+    stats.kernel_launches += 1;
+  }
   RBNS_CUDA(cudaMemsetAsync(u, 0, size_t(B) * m->N * sizeof(double), st));
   stats.kernel_launches += 1;
 
@@ -376,7 +388,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
         // u = 0 at the first step: the convective part vanishes, only the affine block of the GEMM runs
         // (J = L(μ), h = 0); later steps run the full contraction
         const int e = timer.begin(first ? 3 : 0);
-        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first);
+        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first, wts);
         timer.end(e);
         if (rc) break;
         stats.gemm_launches += 1;

@@ -73,6 +73,26 @@ __global__ void init_solve(int32_t* act, int8_t* status, int32_t* iters, double*
   }
 }
 
+// θ weights of the contraction's columns, once per solve (they depend on μ only; SPEC.md:360-368
+// evaluate_weights): W[b][q] = θ_q(μ_b) for the Qb blocks, W[b][Qb + a] = [ν_b] θ_a(μ_b) for the Ql affine
+// columns — the same expressions the contraction prologue evaluates when no table is given.
+__global__ void eval_weights(const double* __restrict__ mu, int64_t B, const rbns_theta_term* __restrict__ thb,
+                             int Qb, const rbns_theta_term* __restrict__ thl, int Ql, int nu_lin,
+                             double* __restrict__ W) {
+  const int ld = Qb + Ql;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B * ld; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / ld;
+    const int q = int(i - b * ld);
+    const double mu0 = mu[2 * b], mu1 = mu[2 * b + 1];
+    if (q < Qb) {
+      W[i] = eval_theta(thb[q], mu0, mu1);
+    } else {
+      const double nu = nu_lin ? 1.0 / mu1 : 1.0;
+      W[i] = nu * eval_theta(thl[q - Qb], mu0, mu1);
+    }
+  }
+}
+
 __global__ void finalize_solve(int8_t* status, int64_t B) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B; i += int64_t(gridDim.x) * blockDim.x)
     if (status[i] == int8_t(kStatusActive)) status[i] = int8_t(RBNS_NON_CONVERGED);

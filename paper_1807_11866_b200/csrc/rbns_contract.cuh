@@ -48,6 +48,7 @@ struct ContractParams {
   int32_t stages;
   double* out;            // [n][ldo]
   int64_t ldo;
+  const double* wts;      // [B][Qb + Ql] precomputed weights (eval_weights), indexed by sample id; NULL = evaluate
 };
 
 #ifndef RBNS_BN
@@ -122,10 +123,16 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     const int i = tile0 + b;
     if (i < p.n) {
       const int id = p.act ? p.act[i] : i;
-      const double mu0 = p.mu[2 * id], mu1 = p.mu[2 * id + 1];
-      const double nu = p.nu_lin ? 1.0 / mu1 : 1.0;
-      for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = eval_theta(p.thb[q], mu0, mu1);
-      for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = nu * eval_theta(p.thl[q], mu0, mu1);
+      if (p.wts) {
+        const double* w = p.wts + int64_t(id) * (p.Qb + p.Ql);
+        for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = w[q];
+        for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = w[p.Qb + q];
+      } else {
+        const double mu0 = p.mu[2 * id], mu1 = p.mu[2 * id + 1];
+        const double nu = p.nu_lin ? 1.0 / mu1 : 1.0;
+        for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = eval_theta(p.thb[q], mu0, mu1);
+        for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = nu * eval_theta(p.thl[q], mu0, mu1);
+      }
     } else {
       for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = 0.0;
       for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = 0.0;
