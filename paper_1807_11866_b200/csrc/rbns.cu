@@ -205,7 +205,7 @@ NewtonParams newton_params(const rbns_model* m) {
 int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
                   const double* mu, int iter, int max_iter, double tol, int32_t* iters, int8_t* status, double* last,
                   int16_t* hints, int32_t* spec_miss, int32_t* miss_list, int32_t* miss_count, int* launches,
-                  bool prefer_rank1, cudaStream_t st) {
+                  bool prefer_rank1, cudaStream_t st, const double* wf = nullptr) {
   if (n <= 0) return RBNS_OK;
   NewtonParams p = newton_params(m);
   p.act = act;
@@ -226,6 +226,7 @@ int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int
   p.miss_list = miss_list;
   p.miss_count = miss_count;
   p.prefer_rank1 = prefer_rank1 ? 1 : 0;
+  p.wf = wf;
   RBNS_CUDA(launch_newton_update(p, st, launches));
   return RBNS_OK;
 }
@@ -365,6 +366,18 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     RBNS_CUDA(cudaGetLastError());
     stats.kernel_launches += 1;
   }
+  // ... and the Newton kernels' residual weights (load terms, group powers)
+  double* wf = nullptr;
+  const int ldf = m->Qf + m->G;
+  if (max_iter > 0) {
+    RBNS_CUDA(ws.alloc(&wf, size_t(B) * ldf * sizeof(double)));
+    LoadWeightParams gp{};
+    gp.G = m->G;
+    for (int g = 0; g < RBNS_MAX_GROUPS; ++g) gp.ge[g] = m->ge[g];
+    eval_load_weights<<<grid_for(B * ldf, 256), 256, 0, st>>>(mu, B, m->thf, m->Qf, gp, wf);
+    RBNS_CUDA(cudaGetLastError());
+    stats.kernel_launches += 1;
+  }
   RBNS_CUDA(cudaMemsetAsync(u, 0, size_t(B) * m->N * sizeof(double), st));
   stats.kernel_launches += 1;
 
@@ -397,7 +410,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
       const int e = timer.begin(1);
       int nl = 0;
       rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, hints,
-                         dcount + 1, miss_list, dcount + 2, &nl, prefer_rank1, st);
+                         dcount + 1, miss_list, dcount + 2, &nl, prefer_rank1, st, wf);
       timer.end(e);
       if (rc) break;
       stats.lu_launches += nl;

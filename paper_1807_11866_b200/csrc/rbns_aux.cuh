@@ -93,6 +93,23 @@ __global__ void eval_weights(const double* __restrict__ mu, int64_t B, const rbn
   }
 }
 
+// The Newton kernels' residual weights, once per solve: W[b] = [θ_f(μ_b) for the Qf load terms, μ₁^{ge[g]} for
+// the G groups] — newton_weights' expressions.
+struct LoadWeightParams {
+  int32_t G;
+  int32_t ge[RBNS_MAX_GROUPS];
+};
+__global__ void eval_load_weights(const double* __restrict__ mu, int64_t B, const rbns_theta_term* __restrict__ thf,
+                                  int Qf, LoadWeightParams gp, double* __restrict__ W) {
+  const int ld = Qf + gp.G;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B * ld; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / ld;
+    const int q = int(i - b * ld);
+    const double mu0 = mu[2 * b], mu1 = mu[2 * b + 1];
+    W[i] = q < Qf ? eval_theta(thf[q], mu0, mu1) : mu1_pow(mu1, gp.ge[q - Qf]);
+  }
+}
+
 __global__ void finalize_solve(int8_t* status, int64_t B) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B; i += int64_t(gridDim.x) * blockDim.x)
     if (status[i] == int8_t(kStatusActive)) status[i] = int8_t(RBNS_NON_CONVERGED);

@@ -48,6 +48,7 @@ struct NewtonParams {
   const int32_t* sub;          // exact kernels: run only the chunk positions sub[0 .. *n_sub) (NULL: all n)
   const int32_t* n_sub;
   int32_t prefer_rank1;        // host policy: pivoting seen, use the hinted rank-1 kernel over the blocked one
+  const double* wf;            // [B][Qf + G] precomputed residual weights (eval_load_weights), or NULL
 };
 
 // CTA → chunk position (and whether this CTA has work) for the exact kernels' optional subset launch
@@ -63,6 +64,12 @@ struct NewtonWeights {
 };
 
 __device__ __forceinline__ void newton_weights(const NewtonParams& p, int b, NewtonWeights& w) {
+  if (p.wf) {  // precomputed once per solve (eval_load_weights): [θ_f(μ_b) …, μ₁^{ge[g]} …]
+    const double* wb = p.wf + int64_t(b) * (p.Qf + p.G);
+    for (int q = threadIdx.x; q < p.Qf; q += blockDim.x) w.th[q] = wb[q];
+    if (threadIdx.x < p.G) w.gf[threadIdx.x] = wb[p.Qf + threadIdx.x];
+    return;
+  }
   const double mu0 = p.mu[2 * b], mu1 = p.mu[2 * b + 1];
   for (int q = threadIdx.x; q < p.Qf; q += blockDim.x) w.th[q] = eval_theta(p.thf[q], mu0, mu1);
   if (threadIdx.x < p.G) w.gf[threadIdx.x] = mu1_pow(mu1, p.ge[threadIdx.x]);
