@@ -115,32 +115,52 @@ __global__ void finalize_solve(int8_t* status, int64_t B) {
     if (status[i] == int8_t(kStatusActive)) status[i] = int8_t(RBNS_NON_CONVERGED);
 }
 
-// K5: stable compaction of the still-active samples (deterministic order).  One CTA of 1024 threads.
+// K5: stable compaction of the still-active samples (deterministic order).  One CTA of 1024 threads; each
+// pass covers 16384 consecutive positions, warp w a contiguous 512-position segment (16 coalesced loads per
+// lane, issued together), ballots give the in-warp order, one shuffle scan the warp offsets.
 constexpr int kCompactThreads = 1024;
 __global__ void __launch_bounds__(kCompactThreads) compact_active(const int32_t* __restrict__ act_in, int32_t n_in,
                                                                    const int8_t* __restrict__ status,
                                                                    int32_t* __restrict__ act_out,
                                                                    int32_t* __restrict__ count) {
-  __shared__ int32_t scan[kCompactThreads];
-  const int tid = threadIdx.x;
-  const int per = (n_in + kCompactThreads - 1) / kCompactThreads;
-  const int beg = min(n_in, tid * per), end = min(n_in, beg + per);
-  int c = 0;
-  for (int i = beg; i < end; ++i) c += status[act_in[i]] == int8_t(kStatusActive);
-  scan[tid] = c;
-  __syncthreads();
-  for (int off = 1; off < kCompactThreads; off <<= 1) {
-    const int v = tid >= off ? scan[tid - off] : 0;
+  constexpr int PER = 16, SEG = 32 * PER, TILE = kCompactThreads * PER;
+  __shared__ int32_t wtot[kCompactThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int running = 0;  // same value in every thread
+  for (int t0 = 0; t0 < n_in; t0 += TILE) {
+    const int s0 = t0 + w * SEG;
+    int32_t id[PER];
+    unsigned m[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = s0 + j * 32 + lane;
+      id[j] = i < n_in ? act_in[i] : -1;
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      m[j] = __ballot_sync(0xffffffffu, id[j] >= 0 && status[id[j]] == int8_t(kStatusActive));
+      cnt += __popc(m[j]);
+    }
+    if (lane == 0) wtot[w] = cnt;
     __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
+    int v = wtot[lane];  // inclusive scan of the 32 warp counts, in every warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    int pos = running + __shfl_sync(0xffffffffu, v, w) - cnt;
+    running += __shfl_sync(0xffffffffu, v, 31);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if ((m[j] >> lane) & 1u) act_out[pos + __popc(m[j] & lt)] = id[j];
+      pos += __popc(m[j]);
+    }
+    __syncthreads();  // wtot is rewritten by the next pass
   }
-  int pos = scan[tid] - c;
-  for (int i = beg; i < end; ++i) {
-    const int32_t id = act_in[i];
-    if (status[id] == int8_t(kStatusActive)) act_out[pos++] = id;
-  }
-  if (tid == kCompactThreads - 1) *count = scan[tid];
+  if (tid == 0) *count = running;
 }
 
 // K4 (second half): p = L^{-T} L^{-1} r per sample, one warp per sample, M_p = L Lᵀ factored once.
