@@ -45,8 +45,16 @@ struct BGJShared {
   signed char rowpos[NB][NR];                    // row -> step c within the panel (or -1)
   signed char pivoted[NR];                       // row already used as a pivot
   double panel[NR * PS];                         // the panel being factored
-  double L[NB][NR][8];                           // −l_{i,c} (negated multipliers), A operand of the DMMA
-  double W[NB][8][8];                            // T⁻¹ (unit lower triangular)
+#ifndef RBNS_BGJ_LS
+#define RBNS_BGJ_LS 8
+#endif
+#ifndef RBNS_BGJ_WS
+#define RBNS_BGJ_WS 10  // 80-byte rows: the four T⁻¹ rows one warp reads per k-step sit in distinct banks
+#endif
+  static constexpr int LS = RBNS_BGJ_LS;         // multiplier row stride (doubles)
+  static constexpr int WS = RBNS_BGJ_WS;         // T⁻¹ row stride (doubles)
+  double L[NB][NR][LS];                          // −l_{i,c} (negated multipliers), A operand of the DMMA
+  double W[NB][8][WS];                           // T⁻¹ (unit lower triangular)
   double Mpi[NW][8][8];                          // per-warp gathered pivot rows of one column tile
   double pivval[NR];
   int perm[NR];
@@ -115,7 +123,7 @@ __device__ __forceinline__ void bgj_factor_spec(int P, int buf, int N, BGJShared
   const int lane = threadIdx.x & 31;
   const int nc = min(8, N - 8 * P);
   if (nc < 8) {  // full panels overwrite every multiplier column
-    for (int e = lane; e < NR * 8; e += 32) (&sh.L[buf][0][0])[e] = 0.0;
+    for (int e = lane; e < NR * BGJShared<RT, CT, NW>::LS; e += 32) (&sh.L[buf][0][0])[e] = 0.0;
     __syncwarp();
   }
   int rr[RPL];
@@ -218,7 +226,7 @@ __device__ __forceinline__ void bgj_factor_pivot(int P, int buf, int N, BGJShare
   for (int c = 0; c < sh.nc[buf]; ++c) sh.rowpos[buf][sh.prow[buf][c]] = -1;  // stale map of panel P-3
   const int nc = min(8, N - 8 * P);
   if (nc < 8) {
-    for (int e = lane; e < NR * 8; e += 32) (&sh.L[buf][0][0])[e] = 0.0;
+    for (int e = lane; e < NR * BGJShared<RT, CT, NW>::LS; e += 32) (&sh.L[buf][0][0])[e] = 0.0;
   }
   double pr[RPL][8];
   unsigned piv_mask = 0;  // bit s: row lane + 32 s already pivoted (or padding)
