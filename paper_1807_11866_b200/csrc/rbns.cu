@@ -629,7 +629,10 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
     op.kalloc = qb * m->Ne + (ql + 3) / 4 * 4;
     op.nchunks = (op.kalloc + 7) / 8;
     op.nsub = op.kalloc / 4;
-    op.stages = 16;
+#ifndef RBNS_STAGES
+#define RBNS_STAGES 16
+#endif
+    op.stages = RBNS_STAGES;  // TMA ring depth (reduced below if shared memory is short)
     while (op.stages > 2 && contract_smem_bytes(op.stages, m->ldu, qb, ql) > size_t(max_smem)) --op.stages;
     op.smem = contract_smem_bytes(op.stages, m->ldu, qb, ql);
     return op.smem <= size_t(max_smem);
