@@ -178,7 +178,9 @@ int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n,
   p.ldo = ldo;
   p.wts = wts;
   const int sample_tiles = (n + kBM - 1) / kBM;
-  const int64_t want = 8LL * m->num_sms;
+  // target CTAs per SM over the launch (16 measured best at configs 1 and 2: 4, 8, 12, 16, 24, 32, 64 tried)
+  static const int64_t waves = env_int64("RBNS_CONTRACT_WAVES", 16);
+  const int64_t want = waves * m->num_sms;
   int groups = int(std::max<int64_t>(1, (want + sample_tiles - 1) / sample_tiles));
   groups = int(std::min<int64_t>(groups, std::max<int64_t>(1, (op.row_tiles + 3) / 4)));
   p.tiles_per_group = int((op.row_tiles + groups - 1) / groups);
