@@ -178,6 +178,35 @@ def test_full_batch_cfg2_properties(cfg_model, dms):
     check_counts(model, mu[pick], it1.cpu().numpy()[pick], itr)
 
 
+def test_full_batch_cfg2_oracle_parity(cfg_model, dms):
+    """Every one of the 65 536 config-2 samples against the oracle (the benchmark's workload): relative error
+    ≤ 1e-10 per sample and identical Newton counts (mismatches only at knife-edge samples).  The oracle runs on
+    all host cores (chunks of 64 μ on a thread pool, BLAS single-threaded per call)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    from threadpoolctl import threadpool_limits
+
+    cfg = synthetic.CONFIGS[2]
+    model = cfg_model(2)
+    dm = dms(2, model)
+    mu = synthetic.config_mu(cfg)
+    u, _, it, st, _, _ = device_solve(dm, mu)
+    S = oracle.symmetrised_operator(model)
+    chunks = range(0, len(mu), 64)
+    with threadpool_limits(1), ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
+        parts = list(ex.map(lambda i: oracle.solve_batch(model, mu[i:i + 64], S=S), chunks))
+    ur = np.concatenate([q[0] for q in parts])
+    itr = np.concatenate([q[1] for q in parts])
+    str_ = np.concatenate([q[2] for q in parts])
+    assert np.all(st == 0) and np.all(str_ == 0)
+    per_sample = np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)
+    assert per_sample.max() <= REL, per_sample.max()
+    mism = np.nonzero(it != itr)[0]
+    assert len(mism) <= 64, len(mism)          # knife-edge cases only (checked below)
+    check_counts(model, mu[mism], it[mism], itr[mism])
+    print(f"cfg2 full batch: max per-sample rel err {per_sample.max():.2e}, count mismatches {len(mism)}")
+
+
 # ---- edge cases the SPEC names -------------------------------------------------------------------------
 
 def _tiny(n=6, q=2, c_scale=0.0, a_scale=1.0, f_scale=1.0, seed=0, **kw):
