@@ -178,19 +178,22 @@ def test_full_batch_cfg2_properties(cfg_model, dms):
     check_counts(model, mu[pick], it1.cpu().numpy()[pick], itr)
 
 
-def test_full_batch_cfg2_oracle_parity(cfg_model, dms):
-    """Every one of the 65 536 config-2 samples against the oracle (the benchmark's workload): relative error
-    ≤ 1e-10 per sample and identical Newton counts (mismatches only at knife-edge samples).  The oracle runs on
-    all host cores (chunks of 64 μ on a thread pool, BLAS single-threaded per call)."""
+@pytest.mark.parametrize("c", [1, 2, 4])
+def test_full_batch_oracle_parity(cfg_model, dms, c):
+    """Every sample of configs 1 (16 384), 2 (65 536: the benchmark's workload) and 4 (65 536, with pressure
+    recovery) against the oracle: relative error ≤ 1e-10 per sample on u (and p) and identical Newton counts
+    (mismatches only at knife-edge samples).  The oracle runs on all host cores (chunks of 64 μ on a thread
+    pool, BLAS single-threaded per call)."""
     import os
     from concurrent.futures import ThreadPoolExecutor
     from threadpoolctl import threadpool_limits
 
-    cfg = synthetic.CONFIGS[2]
-    model = cfg_model(2)
-    dm = dms(2, model)
+    cfg = synthetic.CONFIGS[c]
+    model = cfg_model(c)
+    dm = dms(c, model)
     mu = synthetic.config_mu(cfg)
-    u, _, it, st, _, _ = device_solve(dm, mu)
+    pressure = cfg.n_p > 0
+    u, p, it, st, _, _ = device_solve(dm, mu, pressure=pressure)
     S = oracle.symmetrised_operator(model)
     chunks = range(0, len(mu), 64)
     with threadpool_limits(1), ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
@@ -204,7 +207,13 @@ def test_full_batch_cfg2_oracle_parity(cfg_model, dms):
     mism = np.nonzero(it != itr)[0]
     assert len(mism) <= 64, len(mism)          # knife-edge cases only (checked below)
     check_counts(model, mu[mism], it[mism], itr[mism])
-    print(f"cfg2 full batch: max per-sample rel err {per_sample.max():.2e}, count mismatches {len(mism)}")
+    msg = f"cfg{c} full batch ({len(mu)}): max per-sample rel err u {per_sample.max():.2e}"
+    if pressure:
+        pr = oracle.recover_pressure(model, mu, ur)
+        pe = np.abs(p - pr).max(axis=1) / np.abs(pr).max(axis=1)
+        assert pe.max() <= REL, pe.max()
+        msg += f", p {pe.max():.2e}"
+    print(msg + f", count mismatches {len(mism)}")
 
 
 # ---- edge cases the SPEC names -------------------------------------------------------------------------
