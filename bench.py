@@ -358,7 +358,7 @@ def run_ours(args, cfg, world, rank, local):
                 "roofline": roof, "roofline_e2e": roof_e2e, "newton_update": newton, "gpu_launches": launches, "clocks": clocks.summary(),
                 "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
                            "converged": int((res.status == 0).sum().item()), "batch": batch}}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is timed at N = 1 only
             line["cpu_baseline"] = cpu_baseline(cfg, model, mu_np, min(args.cpu_sample, batch))
         print(json.dumps(line), flush=True)
     dm.close()
