@@ -182,7 +182,8 @@ int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n,
   static const int64_t waves = env_int64("RBNS_CONTRACT_WAVES", 16);
   const int64_t want = waves * m->num_sms;
   int groups = int(std::max<int64_t>(1, (want + sample_tiles - 1) / sample_tiles));
-  groups = int(std::min<int64_t>(groups, std::max<int64_t>(1, (op.row_tiles + 3) / 4)));
+  static const int64_t min_tiles = std::max<int64_t>(1, env_int64("RBNS_CONTRACT_MIN_TILES", 4));  // per CTA
+  groups = int(std::min<int64_t>(groups, std::max<int64_t>(1, (op.row_tiles + min_tiles - 1) / min_tiles)));
   p.tiles_per_group = int((op.row_tiles + groups - 1) / groups);
   groups = int((op.row_tiles + p.tiles_per_group - 1) / p.tiles_per_group);
   dim3 grid(sample_tiles, groups);
