@@ -111,11 +111,10 @@ const BShape* bplan(int N) {
   return nullptr;
 }
 
-// RBNS_NEWTON=bgj selects the blocked DMMA kernel (rbns_bgj.cuh); the default is the rank-1 register kernel
-// (rbns_newton.cuh), currently the faster of the two at N ≤ 104 (both are parity-tested).
-// The blocked kernel is the default where it measured faster (88 < N ≤ 103: cfg-2 Newton update 78 ms vs 89 ms
-// for the speculative rank-1 kernel); RBNS_NEWTON=bgj forces it for every N it covers, any other RBNS_NEWTON
-// value forces the rank-1 kernels.
+// Kernel choice: the blocked DMMA kernel (rbns_bgj.cuh) is the default where it measured faster (88 < N ≤ 103:
+// cfg-2 Newton update 74 ms against 89 ms for the speculative rank-1 kernel); elsewhere the rank-1 register
+// kernels (rbns_newton*.cuh) run.  RBNS_NEWTON=bgj forces the blocked kernel for every N it covers, any other
+// RBNS_NEWTON value forces the rank-1 kernels (all are parity-tested).
 bool use_blocked(int N) {
   static const int mode = [] {
     const char* v = std::getenv("RBNS_NEWTON");
