@@ -178,29 +178,46 @@ def test_full_batch_cfg2_properties(cfg_model, dms):
     check_counts(model, mu[pick], it1.cpu().numpy()[pick], itr)
 
 
+def threaded_oracle(model, mu, chunk=64):
+    """oracle.solve_batch over all host cores: chunks of μ on a thread pool, BLAS single-threaded per call."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    from threadpoolctl import threadpool_limits
+
+    S = oracle.symmetrised_operator(model)
+    with threadpool_limits(1), ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
+        parts = list(ex.map(lambda i: oracle.solve_batch(model, mu[i:i + chunk], S=S), range(0, len(mu), chunk)))
+    return tuple(np.concatenate([q[k] for q in parts]) for k in range(3))
+
+
+def test_cfg3_slice_oracle_parity(cfg_model, dms):
+    """Config 3 (N = 200, Q = 13: the 2-CTA cluster Newton kernel, S streamed from HBM) on a 1024-sample slice."""
+    cfg = synthetic.CONFIGS[3]
+    model = cfg_model(3)
+    mu = synthetic.config_mu(cfg, 1024)
+    u, _, it, st, _, _ = device_solve(dms(3, model), mu)
+    ur, itr, str_ = threaded_oracle(model, mu, chunk=16)
+    assert np.all(st == 0) and np.all(str_ == 0)
+    per_sample = np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)
+    assert per_sample.max() <= REL, per_sample.max()
+    mism = np.nonzero(it != itr)[0]
+    check_counts(model, mu[mism], it[mism], itr[mism])
+    print(f"cfg3 slice (1024): max per-sample rel err u {per_sample.max():.2e}, count mismatches {len(mism)}")
+
+
 @pytest.mark.parametrize("c", [1, 2, 4])
 def test_full_batch_oracle_parity(cfg_model, dms, c):
     """Every sample of configs 1 (16 384), 2 (65 536: the benchmark's workload) and 4 (65 536, with pressure
     recovery) against the oracle: relative error ≤ 1e-10 per sample on u (and p) and identical Newton counts
     (mismatches only at knife-edge samples).  The oracle runs on all host cores (chunks of 64 μ on a thread
     pool, BLAS single-threaded per call)."""
-    import os
-    from concurrent.futures import ThreadPoolExecutor
-    from threadpoolctl import threadpool_limits
-
     cfg = synthetic.CONFIGS[c]
     model = cfg_model(c)
     dm = dms(c, model)
     mu = synthetic.config_mu(cfg)
     pressure = cfg.n_p > 0
     u, p, it, st, _, _ = device_solve(dm, mu, pressure=pressure)
-    S = oracle.symmetrised_operator(model)
-    chunks = range(0, len(mu), 64)
-    with threadpool_limits(1), ThreadPoolExecutor(len(os.sched_getaffinity(0))) as ex:
-        parts = list(ex.map(lambda i: oracle.solve_batch(model, mu[i:i + 64], S=S), chunks))
-    ur = np.concatenate([q[0] for q in parts])
-    itr = np.concatenate([q[1] for q in parts])
-    str_ = np.concatenate([q[2] for q in parts])
+    ur, itr, str_ = threaded_oracle(model, mu)
     assert np.all(st == 0) and np.all(str_ == 0)
     per_sample = np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)
     assert per_sample.max() <= REL, per_sample.max()
