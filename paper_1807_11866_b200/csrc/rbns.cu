@@ -131,6 +131,7 @@ struct rbns_model {
   int Qa = 0, Qc = 0, Qf = 0, Qp = 0;      // family sizes: linear, quadratic, load, coupling
   int G = 0, ge[RBNS_MAX_GROUPS] = {};     // h groups and their μ₁ exponents
   int nu_lin = 0;
+  int jl = 0;                              // J block layout the Newton kernels read (jidx)
   int n_stop = 0, stop_abs = 0;            // stop norm over the leading n_stop unknowns; absolute or relative
   Operand vel, prs;
   double* f = nullptr;                     // [Qf][N]
@@ -202,6 +203,8 @@ NewtonParams newton_params(const rbns_model* m) {
   for (int g = 0; g < RBNS_MAX_GROUPS; ++g) p.ge[g] = m->ge[g];
   p.n_stop = m->n_stop;
   p.stop_abs = m->stop_abs;
+  p.jl = m->jl;
+  p.num_sms = m->num_sms;
   return p;
 }
 
@@ -617,6 +620,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   m->G = int(ge.size());
   for (int g = 0; g < m->G; ++g) m->ge[g] = ge[g];
   m->Ne = (m->N + 3) / 4 * 4;  // κ stride per block (k4 sub-steps never straddle)
+  m->jl = newton_layout(m->N);
   m->ldu = contract_ldu(m->Ne);
   auto cleanup = [&](int rc) {
     rbns_model_destroy(m);
@@ -649,6 +653,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   // model created later with a smaller tile cannot invalidate launches of an earlier one
   if (cudaFuncSetAttribute(kContract, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem) != cudaSuccess)
     return cleanup(fail(RBNS_ERR_CUDA, "cudaFuncSetAttribute(contract) failed"));
+  if (newton_prepare(m->N) != cudaSuccess) return cleanup(fail(RBNS_ERR_CUDA, "Newton kernel attributes failed"));
 
   // keep freed stream-ordered allocations pooled (no re-allocation between calls)
   cudaMemPool_t pool;
@@ -704,7 +709,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
             step(cudaMalloc(&m->vel.S, size_t(m->vel.rows) * m->vel.kalloc * sizeof(double)), "cudaMalloc(S)");
   if (ok) {
     build_velocity_operator<<<4 * m->num_sms, 256>>>(m->vel.S, m->vel.rows, m->vel.kalloc, dC, Qc, dA, Qa, dhb, dhg,
-                                                     drho, m->N, m->Ne, Qb);
+                                                     drho, m->N, m->Ne, Qb, m->jl);
     ok = step(cudaGetLastError(), "build_velocity_operator") && step(cudaDeviceSynchronize(), "build S");
   }
   for (void* ptr : {static_cast<void*>(dC), static_cast<void*>(dA), static_cast<void*>(dhb),

@@ -13,7 +13,7 @@ namespace rbns {
 __global__ void build_velocity_operator(double* __restrict__ S, int64_t rows, int kalloc,
                                         const double* __restrict__ C, int Qc, const double* __restrict__ A, int Ql,
                                         const int* __restrict__ hb, const int* __restrict__ hg,
-                                        const double* __restrict__ rho, int N, int Ne, int Qb) {
+                                        const double* __restrict__ rho, int N, int Ne, int Qb, int jl) {
   const int64_t total = rows * kalloc;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
@@ -22,7 +22,8 @@ __global__ void build_velocity_operator(double* __restrict__ S, int64_t rows, in
     double v = 0.0;
     const int64_t nn = int64_t(N) * N;
     if (r < nn) {
-      const int l = int(r / N), m = int(r - int64_t(l) * N);
+      int l, m;  // S row r carries J[l][m] at its position in the model's J layout
+      jpos(r, N, jl, l, m);
       if (kap < Qc * Ne) {
         const int q = kap / Ne, k = kap - q * Ne;
         if (k < N) {
@@ -236,10 +237,13 @@ __global__ void operator_readout(const double* __restrict__ Y, int64_t ldy, cons
   __syncthreads();
   const int N = p.N;
   const double* Yb = Y + int64_t(b) * ldy;
-  for (int64_t e = threadIdx.x; e < int64_t(N) * N; e += blockDim.x) Jout[int64_t(b) * N * N + e] = Yb[e];
+  for (int64_t e = threadIdx.x; e < int64_t(N) * N; e += blockDim.x) {
+    const int l = int(e / N), m = int(e - int64_t(l) * N);
+    Jout[int64_t(b) * N * N + e] = Yb[jidx(l, m, N, p.jl)];
+  }
   for (int l = threadIdx.x; l < N; l += blockDim.x) {
     double ju = 0.0;
-    for (int m = 0; m < N; ++m) ju = fma(Yb[int64_t(l) * N + m], eta[int64_t(b) * N + m], ju);
+    for (int m = 0; m < N; ++m) ju = fma(Yb[jidx(l, m, N, p.jl)], eta[int64_t(b) * N + m], ju);
     R[int64_t(b) * N + l] = -newton_rhs(p, Yb, l, ju, w);
   }
 }

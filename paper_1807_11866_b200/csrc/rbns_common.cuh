@@ -123,6 +123,67 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
+// 1-D bulk copy global -> shared (TMA engine), completion signalled on an mbarrier (transaction bytes).
+// 16-byte aligned addresses, size % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+
+// orders this thread's earlier generic-proxy shared-memory accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// Jacobian block layouts (the contraction writes J in the layout its Newton kernel reads; NewtonParams::jl)
+//   0  row-major: J[l][m] at l·N + m
+//   1  tile layout of the tiled Gauss–Jordan kernel (rbns_tgj.cuh): 8×8 tiles (row tile i = l/8, column
+//      tile j = m/8) stored column-tile-major, row tiles in order inside a column tile, and inside a tile
+//      column-major (g = m%8 outer, ts = l%8 inner) over the tile's real rows rr and columns cr only.  A full
+//      tile is 64 contiguous doubles in which lane (g, t) of the DMMA fragment layout finds its pair
+//      (rows 8i+2t, 8i+2t+1 of column 8j+g) at offset 2·lane: one 16-byte load per lane, no padding bytes.
+//      The h rows (residual helpers) follow at N² + g·N + l in both layouts.
+// ---------------------------------------------------------------------------------------------------------
+__host__ __device__ inline int64_t jidx_tile(int l, int m, int N) {
+  const int i = l >> 3, ts = l & 7, j = m >> 3, g = m & 7;
+  const int rr = N - 8 * i < 8 ? N - 8 * i : 8;
+  const int cr = N - 8 * j < 8 ? N - 8 * j : 8;
+  return int64_t(8 * j) * N + int64_t(8 * i) * cr + g * rr + ts;
+}
+
+__host__ __device__ inline int64_t jidx(int l, int m, int N, int jl) {
+  return jl ? jidx_tile(l, m, N) : int64_t(l) * N + m;
+}
+
+// inverse of jidx: position r < N² -> (l, m)
+__host__ __device__ inline void jpos(int64_t r, int N, int jl, int& l, int& m) {
+  if (!jl) {
+    l = int(r / N);
+    m = int(r - int64_t(l) * N);
+    return;
+  }
+  const int j = int(r / (8 * int64_t(N)));
+  const int rem = int(r - int64_t(8 * j) * N);
+  const int cr = N - 8 * j < 8 ? N - 8 * j : 8;
+  const int i = rem / (8 * cr);
+  const int rem2 = rem - 8 * i * cr;
+  const int rr = N - 8 * i < 8 ? N - 8 * i : 8;
+  const int g = rem2 / rr;
+  l = 8 * i + (rem2 - g * rr);
+  m = 8 * j + g;
+}
+
 // FP64 tensor-core MMA (lowers to DMMA.8x8x4 on sm_100a): D(8x8) += A(8x4) * B(4x8).
 // Thread (g = lane>>2, t = lane&3) supplies A[g][t], B[t][g]; holds D[g][2t], D[g][2t+1].
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {

@@ -10,6 +10,10 @@ namespace rbns {
 struct NewtonParams;
 
 bool newton_supported(int N);
+// J block layout the Newton kernels for N read (jidx): 1 when the tiled Gauss–Jordan kernel handles N
+int newton_layout(int N);
+// per-device setup (function attributes) for the Newton kernels of size N; call with the model's device current
+cudaError_t newton_prepare(int N);
 // launches the Newton-update kernel(s) for p on st; *launches receives the number of kernels launched
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches);
 

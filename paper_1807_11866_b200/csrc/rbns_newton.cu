@@ -12,6 +12,7 @@
 #include "rbns_newton3.cuh"
 #include "rbns_newton_spec.cuh"
 #include "rbns_newton_cluster.cuh"
+#include "rbns_tgj.cuh"
 
 namespace rbns {
 
@@ -123,6 +124,30 @@ bool use_blocked(int N) {
   }();
   return mode == 1 || (mode == 0 && N > 88 && N <= 103);
 }
+
+// tiled Gauss–Jordan kernel (rbns_tgj.cuh): RT = ⌈N/8⌉ row tiles, CT = ⌈(N+1)/8⌉ column tiles, NW warps
+struct TShape {
+  int rt, ct, nw;
+  NewtonKernel kern;
+  size_t base;  // shared memory before the J staging buffer
+};
+#define RBNS_TS(R_, C_, W_) {R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>()}
+const TShape kTShapes[] = {
+    RBNS_TS(13, 13, 4),  // 96 < N ≤ 103 (config 2 / 4: N = 100)
+};
+#undef RBNS_TS
+
+const TShape* tplan(int N) {
+  static const bool off = [] {  // any RBNS_NEWTON value other than "tgj" selects the earlier kernels
+    const char* v = std::getenv("RBNS_NEWTON");
+    return v && *v && std::strcmp(v, "tgj") != 0;
+  }();
+  if (off || N <= 8) return nullptr;
+  const int rt = (N + 7) / 8, ct = (N + 8) / 8;
+  for (const TShape& s : kTShapes)
+    if (s.rt == rt && s.ct == ct) return &s;
+  return nullptr;
+}
 }  // namespace
 
 // N > 127: the 2-CTA cluster kernel (rbns_newton_cluster.cuh), 16×(2×16) threads, N ≤ 207
@@ -130,17 +155,55 @@ constexpr int kClusterMaxN = 207;
 
 bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
 
+int newton_layout(int N) { return tplan(N) != nullptr ? 1 : 0; }
+
+cudaError_t newton_prepare(int N) {
+  int dev = 0, max_smem = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  // per-device function attributes (cudaFuncSetAttribute applies to the current device only)
+  if (const TShape* t = tplan(N)) {
+    e = cudaFuncSetAttribute(t->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(t->kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  if (const BShape* b = bplan(N)) {
+    e = cudaFuncSetAttribute(b->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(b->smem));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// the exact full-search kernel over the samples a speculative pass listed (device-side count)
+static cudaError_t launch_exact(const Shape* s, const NewtonParams& p, cudaStream_t st) {
+  NewtonParams q = p;
+  q.sub = p.miss_list;
+  q.n_sub = p.miss_count;
+  s->exact<<<std::min(p.n, 2 * p.num_sms), s->tgr * s->tgc, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches) {
   *launches = 1;
-  if (!p.prefer_rank1 && use_blocked(p.N)) {
+  if (!p.prefer_rank1 && p.jl) {
+    const TShape* t = tplan(p.N);
+    const Shape* s = plan(p.N);
+    if (t && s && s->exact) {
+      cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
+      if (e != cudaSuccess) return e;
+      const size_t smem = t->base + size_t(p.ldj) * sizeof(double);
+      t->kern<<<std::min(p.n, 2 * p.num_sms), t->nw * 32, smem, st>>>(p);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      *launches = 2;
+      return launch_exact(s, p, st);
+    }
+  }
+  if (!p.prefer_rank1 && !p.jl && use_blocked(p.N)) {
     if (const BShape* b = bplan(p.N)) {
-      static bool attr_set[sizeof(kBShapes) / sizeof(kBShapes[0])] = {};
-      const int idx = int(b - kBShapes);
-      if (!attr_set[idx]) {  // benign race: idempotent attribute
-        cudaError_t e = cudaFuncSetAttribute(b->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(b->smem));
-        if (e != cudaSuccess) return e;
-        attr_set[idx] = true;
-      }
       b->kern<<<p.n, b->nw * 32, b->smem, st>>>(p);
       return cudaGetLastError();
     }
@@ -151,31 +214,17 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
     return cudaGetLastError();
   }
   if (!s) return cudaErrorInvalidValue;
-#ifdef RBNS_GJ_ONE_CTA_PER_SM  // development experiment: force one CTA per SM through unused shared memory
-  static bool set1 = false;
-  if (!set1) { cudaFuncSetAttribute(s->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024); set1 = true; }
-  s->kern<<<p.n, s->tgr * s->tgc, 150 * 1024, st>>>(p);
-#else
   if (s->exact) {
     // speculative pass, then the exact kernel over the samples it handed back (device-side count)
     cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
-    NewtonParams q = p;
-    q.sub = p.miss_list;
-    q.n_sub = p.miss_count;
-    static const int sms = [] {
-      int dev = 0, v = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-      return v;
-    }();
-    s->exact<<<std::min(p.n, 2 * sms), s->tgr * s->tgc, 0, st>>>(q);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     *launches = 2;
-  } else {
-    s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
+    return launch_exact(s, p, st);
   }
-#endif
+  s->kern<<<p.n, s->tgr * s->tgc, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,8 @@ struct NewtonParams {
   const int32_t* n_sub;
   int32_t prefer_rank1;        // host policy: pivoting seen, use the hinted rank-1 kernel over the blocked one
   const double* wf;            // [B][Qf + G] precomputed residual weights (eval_load_weights), or NULL
+  int32_t jl;                  // layout of the J block (jidx, rbns_common.cuh): 0 row-major, 1 tile layout
+  int32_t num_sms;             // SMs of the model's device (persistent / subset grids)
 };
 
 // CTA → chunk position (and whether this CTA has work) for the exact kernels' optional subset launch

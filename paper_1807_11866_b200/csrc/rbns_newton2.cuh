@@ -180,7 +180,7 @@ __device__ __forceinline__ void gj_load_system(const NewtonParams& p, int i_s, i
 #pragma unroll
     for (int s = 0; s < CS; ++s) {
       const int i = tr + TGR * r, j = tc + TGC * s;
-      a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
+      a[r][s] = (i < N && j < N) ? __ldcs(&Jb[jidx(i, j, N, p.jl)]) : 0.0;
     }
   double uj[CS];
 #pragma unroll

@@ -264,7 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
   #pragma unroll
       for (int s = 0; s < CS; ++s) {
         const int i = tr + TGR * r, j = gcol(s);
-        a[r][s] = (i < N && j < N) ? __ldcs(&Jb[int64_t(i) * N + j]) : 0.0;
+        a[r][s] = (i < N && j < N) ? __ldcs(&Jb[jidx(i, j, N, p.jl)]) : 0.0;
       }
 
     // right-hand side −R = f − ½ J u − ½ L(μ)u as column N (owned by CTA rhs_rank)
