@@ -54,6 +54,17 @@ __host__ __device__ constexpr int tgj_slot(int r, int c) {
 }
 
 
+#ifdef RBNS_TRACE  // clock64 trace of sample 0 (tools/trace_tgj.py)
+#define TGJ_TR(slot)                                                   \
+  do {                                                                 \
+    if (i_s == 2960 && (threadIdx.x & 31) == 0) g_trace[(slot) & 255] = clock64(); /* a steady-state sample */ \
+  } while (0)
+#else
+#define TGJ_TR(slot) \
+  do {               \
+  } while (0)
+#endif
+
 constexpr int kTgjSlots = 3;  // panel buffers in flight (published → consumed by every warp)
 
 template <int RT, int NW>
@@ -67,7 +78,7 @@ struct TGJShared {
                                      // prologue's per-warp row sums of J u alias it
   double rhs[NR];                    // right-hand side, then the unscaled solution column
   double red[2][NW];
-  uint64_t full[NB], empty[NB];      // panel slots: published (one arrival) / consumed (one per warp)
+  uint64_t full[NB], empty[NB];      // panel slot: every M_i published (one arrival) / consumed (one per warp)
   uint64_t bar;                      // staging buffer: the next sample's J block has landed
   int fail;                          // current sample: rejected speculation or unusable pivot
 };
@@ -120,37 +131,70 @@ __device__ __forceinline__ TgjPivot tgj_invert(double a0, double a1, int nc) {
   return TgjPivot{e0, e1, l0, l1, __any_sync(0xffffffffu, bad) != 0};
 }
 
-// Row tile P of a register column tile (P is CTA-uniform: ⌈log2 RT⌉ uniform branches, static registers).
-template <int LO, int HI, int RT>
+// Row tile P of a register column tile: a branch-free select tree on the bits of P (CTA-uniform), static
+// register indices, ⌈log2 RT⌉ levels of independent selects.
+template <int RT>
 __device__ __forceinline__ void tgj_pick(const double (&a)[RT][2], int P, double& p0, double& p1) {
-  if constexpr (HI - LO == 1) {
-    p0 = a[LO][0];
-    p1 = a[LO][1];
-  } else {
-    constexpr int MID = (LO + HI) / 2;
-    if (P < MID)
-      tgj_pick<LO, MID, RT>(a, P, p0, p1);
-    else
-      tgj_pick<MID, HI, RT>(a, P, p0, p1);
+  constexpr int NP2 = RT <= 2 ? 2 : RT <= 4 ? 4 : RT <= 8 ? 8 : 16;
+  double v0[NP2], v1[NP2];
+#pragma unroll
+  for (int i = 0; i < NP2; ++i) {
+    v0[i] = a[i < RT ? i : RT - 1][0];
+    v1[i] = a[i < RT ? i : RT - 1][1];
   }
+#pragma unroll
+  for (int w = NP2 / 2, bit = 0; w >= 1; w >>= 1, ++bit) {
+    const bool hi = (P >> bit) & 1;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      v0[i] = hi ? v0[2 * i + 1] : v0[2 * i];
+      v1[i] = hi ? v1[2 * i + 1] : v1[2 * i];
+    }
+  }
+  p0 = v0[0];
+  p1 = v1[0];
 }
 
-// Panel P (W fragment wv = row g of W_P, pivot column M) applied to one register column tile a, unscaled:
-// X = (J_Pj)ᵀ Wᵀ, then (J_ij)ᵀ += X M_iᵀ for every i (M_P = 0 leaves the pivot row tile as it is).
+// X_Pjᵀ = (J_Pj)ᵀ Wᵀ for one register column tile (W fragment wv = row g of W_P): the panel's scaled pivot
+// row tile, k-permuted C fragment (k-step s of the next product uses element s).
 template <int RT>
-__device__ __forceinline__ void tgj_apply(double (&a)[RT][2], int P, const double2 wv, const double (*M)[64]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+__device__ __forceinline__ void tgj_x(const double (&a)[RT][2], int P, const double2 wv, double& x0, double& x1) {
   double p0, p1;
-  tgj_pick<0, RT, RT>(a, P, p0, p1);
-  double x0 = 0.0, x1 = 0.0;
+  tgj_pick<RT>(a, P, p0, p1);
+  x0 = x1 = 0.0;
   dmma_8x8x4(x0, x1, p0, wv.x);
   dmma_8x8x4(x0, x1, p1, wv.y);
+}
+
+// (J_ij)ᵀ += X M_iᵀ for every row tile i (unscaled Gauss–Jordan: M_P = 0 leaves the pivot row tile as it is).
+template <int RT>
+__device__ __forceinline__ void tgj_update(double (&a)[RT][2], double x0, double x1, const double (*M)[64]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int i = 0; i < RT; ++i) {
     const double2 m = *reinterpret_cast<const double2*>(&M[i][tgj_slot(g, 2 * t)]);
     dmma_8x8x4(a[i][0], a[i][1], x0, m.x);
     dmma_8x8x4(a[i][0], a[i][1], x1, m.y);
   }
+}
+
+// Panel P (W fragment wv, pivot column M) applied to one register column tile.
+template <int RT>
+__device__ __forceinline__ void tgj_apply(double (&a)[RT][2], int P, const double2 wv, const double (*M)[64]) {
+  double x0, x1;
+  tgj_x<RT>(a, P, wv, x0, x1);
+  tgj_update<RT>(a, x0, x1, M);
+}
+
+// (row tile i of a) + X M_iᵀ into (q0, q1), a left unchanged
+template <int RT>
+__device__ __forceinline__ void tgj_row(const double (&a)[RT][2], int i, double x0, double x1, const double* Mi,
+                                        double& q0, double& q1) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  tgj_pick<RT>(a, i, q0, q1);
+  const double2 m = *reinterpret_cast<const double2*>(&Mi[tgj_slot(g, 2 * t)]);
+  dmma_8x8x4(q0, q1, x0, m.x);
+  dmma_8x8x4(q0, q1, x1, m.y);
 }
 
 // Verification of panel P for this warp's share of the rows below its pivot tile (row tiles i > P,
@@ -165,30 +209,31 @@ __device__ __forceinline__ bool tgj_verify(int P, int NP, int N, const double2 w
   dmma_8x8x4(ui0, ui1, Ls[tgj_slot(2 * t, g)], wv.x);
   dmma_8x8x4(ui0, ui1, Ls[tgj_slot(2 * t + 1, g)], wv.y);
   bool bad = false;
-#pragma unroll 1
-  for (int i = i0; i < NP; i += NW) {
-    const double2 m = *reinterpret_cast<const double2*>(&M[i][tgj_slot(g, 2 * t)]);
-    double l0 = 0.0, l1 = 0.0;
-    dmma_8x8x4(l0, l1, m.x, ui0);
-    dmma_8x8x4(l0, l1, m.y, ui1);
-    bad |= 8 * i + g < N && (fabs(l0) > 1.0 || fabs(l1) > 1.0);
+  constexpr int MAXI = (16 + NW - 1) / NW;
+#pragma unroll
+  for (int k = 0; k < MAXI; ++k) {
+    const int i = i0 + k * NW;
+    if (i < NP) {
+      const double2 m = *reinterpret_cast<const double2*>(&M[i][tgj_slot(g, 2 * t)]);
+      double l0 = 0.0, l1 = 0.0;
+      dmma_8x8x4(l0, l1, m.x, ui0);
+      dmma_8x8x4(l0, l1, m.y, ui1);
+      bad |= 8 * i + g < N && (fabs(l0) > 1.0 || fabs(l1) > 1.0);
+    }
   }
   return __any_sync(0xffffffffu, bad) != 0;
 }
 
-// residual entry r: f(μ)_r − ½ (J u)_r − ½ (L(μ) u)_r, weights from the per-solve table (eval_load_weights)
-// or evaluated here, h rows from the staging buffer
-__device__ __forceinline__ double tgj_rhs(const NewtonParams& p, int b, const double* jst, int r, double ju) {
-  const int N = p.N;
-  const double mu0 = p.mu[2 * b], mu1 = p.mu[2 * b + 1];
+// load part of the residual, f(μ)_r, and the h-group weights μ₁^{e_g} (independent of J: evaluated while the
+// sample's J block is still in flight); weights from the per-solve table (eval_load_weights) or evaluated here
+__device__ __forceinline__ double tgj_load_term(const NewtonParams& p, int b, int r) {
   const double* wb = p.wf ? p.wf + int64_t(b) * (p.Qf + p.G) : nullptr;
+  const double mu0 = p.mu[2 * b], mu1 = p.mu[2 * b + 1];
   double fi = 0.0;
 #pragma unroll 4
   for (int q = 0; q < p.Qf; ++q)
-    fi = fma(wb ? wb[q] : eval_theta(p.thf[q], mu0, mu1), __ldg(&p.f[q * N + r]), fi);
-  double h = 0.0;
-  for (int gg = 0; gg < p.G; ++gg) h = fma(wb ? wb[p.Qf + gg] : mu1_pow(mu1, p.ge[gg]), jst[N * N + gg * N + r], h);
-  return fi - 0.5 * ju - 0.5 * h;
+    fi = fma(wb ? wb[q] : eval_theta(p.thf[q], mu0, mu1), __ldg(&p.f[q * p.N + r]), fi);
+  return fi;
 }
 
 template <int RT, int CT, int NW>
@@ -236,12 +281,31 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
   for (int i_s = blockIdx.x; i_s < p.n; i_s += gridDim.x) {
     const int b = p.act[i_s];
     const int nxt_s = i_s + int(gridDim.x);
+    // J-independent work first, while the block may still be in flight: pivot-order hint, f(μ), weights, u
     bool ident = true;
     if (p.hint_in)
       for (int k = tid; k < N; k += NT) ident &= p.hint_in[int64_t(b) * N + k] == k;
+    static_assert(NR <= NT, "one row per thread");
+    const double fr = tid < N ? tgj_load_term(p, b, tid) : 0.0;
+    double hw[RBNS_MAX_GROUPS];
+#pragma unroll
+    for (int gg = 0; gg < RBNS_MAX_GROUPS; ++gg)
+      hw[gg] = gg < p.G ? (p.wf ? p.wf[int64_t(b) * (p.Qf + p.G) + p.Qf + gg] : mu1_pow(p.mu[2 * b + 1], p.ge[gg]))
+                        : 0.0;
+    double u0[8];  // column tile 0 of u (every thread)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) u0[c] = p.u[int64_t(b) * N + c];
+    double uj[JJ];  // this lane's columns of u in its owned tiles
+#pragma unroll
+    for (int jj = 0; jj < JJ; ++jj) {
+      const int col = 8 * (1 + warp + NW * jj) + g;
+      uj[jj] = col < N ? p.u[int64_t(b) * N + col] : 0.0;
+    }
     if (tid == 0) sh.fail = 0;
+    TGJ_TR(0);
     mbar_wait(&sh.bar, phase);
     phase ^= 1u;
+    TGJ_TR(1);
     if (!__syncthreads_and(ident)) {  // interchanges at the previous iteration: the exact kernel takes it
       if (tid == 0) {
         p.miss_list[atomicAdd(p.miss_count, 1)] = i_s;
@@ -280,15 +344,10 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
       }
     }
 
+    TGJ_TR(5);
     // ---- right-hand side −R = f − ½ J u − ½ L(μ)u: per-lane partial row sums over the warp's columns,
     //      reduced over the 8 column lanes g by a reduce-scatter (16 + 8 + 4 shuffles for 32 values) ----
     {
-      double uj[JJ];
-#pragma unroll
-      for (int jj = 0; jj < JJ; ++jj) {
-        const int col = 8 * (1 + warp + NW * jj) + g;
-        uj[jj] = col < N ? p.u[int64_t(b) * N + col] : 0.0;
-      }
       double v[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) v[k] = 0.0;
@@ -315,8 +374,11 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
         if (kk < 2 * RT) rowred[warp][8 * (kk >> 1) + 2 * t + (kk & 1)] = v[k];
       }
     }
+    TGJ_TR(6);
     __syncthreads();
-    for (int r = tid; r < NR; r += NT) {
+    TGJ_TR(7);
+    if (tid < NR) {
+      const int r = tid;
       double rhs = 0.0;
       if (r < N) {
         double ju = 0.0;
@@ -325,11 +387,16 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
         const int i = r >> 3, rr = N - 8 * i < 8 ? N - 8 * i : 8;
         const double* tb = jst + 64 * i;  // column tile 0 (N > 8: 8 columns)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) ju = fma(tb[c * rr + (r & 7)], p.u[int64_t(b) * N + c], ju);
-        rhs = tgj_rhs(p, b, jst, r, ju);
+        for (int c = 0; c < 8; ++c) ju = fma(tb[c * rr + (r & 7)], u0[c], ju);
+        double h = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < RBNS_MAX_GROUPS; ++gg)
+          if (gg < p.G) h = fma(hw[gg], jst[N * N + gg * N + r], h);
+        rhs = fr - 0.5 * ju - 0.5 * h;
       }
       sh.rhs[r] = rhs;
     }
+    TGJ_TR(8);
     // panel 0 (column tile 0, shared memory only): M_i = −J_i0, M_0 = 0, transposed into the slot layout
     const int s0 = pc0 % NB;
     for (int e = tid; e < RT * 64; e += NT) {
@@ -343,7 +410,9 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
       d0 = v.x;
       d1 = v.y;
     }
+    TGJ_TR(2);
     __syncthreads();  // the staging buffer is consumed: stage the next sample behind the elimination
+    TGJ_TR(3);
     if (tid == 0 && nxt_s < p.n) {
       fence_proxy_async_smem();
       issue(nxt_s);
@@ -371,6 +440,7 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
         if (pv.bad) sh.fail = 1;
         mbar_arrive(&sh.full[s0]);
       }
+      TGJ_TR(4);
     }
 
     // ---- blocked Gauss–Jordan over the panels (dataflow through the panel slots) ----
@@ -388,26 +458,40 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
       if (tgj_verify<NW>(P, NP, N, wv, sh.L[s], sh.M[s]) && lane == 0) sh.fail = 1;
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.empty[s]);
+      TGJ_TR(64 + 4 * P + warp);
     };
 #pragma unroll 1
     for (int P = 0; P < NP; ++P) {
       const int pc = pc0 + P, s = pc % NB;
-      mbar_wait(&sh.full[s], (uint32_t(pc) / NB) & 1u);
+      const uint32_t par = (uint32_t(pc) / NB) & 1u;
       const int nx = P + 1;
-      if (nx < NP && warp == (nx - 1) % NW) {
+      const bool own1 = nx < NP && warp == (nx - 1) % NW;
+      mbar_wait(&sh.full[s], par);
+      TGJ_TR(128 + 4 * P + warp);
+      if (own1) {
+        // critical path: panel P into tile nx, the inverse of its new pivot tile, publication of panel nx
         const int jn = (nx - 1) / NW;
         const double2 wv = *reinterpret_cast<const double2*>(&sh.W[s][tgj_slot(g, 2 * t)]);
+        const int s1 = (pc + 1) % NB;
+        const int nc = nx == NP - 1 ? ncl : 8;
+        const bool live_col = g < nc;
 #pragma unroll
         for (int jj = 0; jj < JJ; ++jj) {
           if (jj != jn) continue;
-          tgj_apply<RT>(acc[jj], P, wv, sh.M[s]);
-          double q0, q1;
-          tgj_pick<0, RT, RT>(acc[jj], nx, q0, q1);
-          const TgjPivot pv = tgj_invert(q0, q1, nx == NP - 1 ? ncl : 8);
-          const int s1 = (pc + 1) % NB;
+          // (ordering note: the inversion follows the tile update; with the inversion placed between X and the
+          // update, ptxas -O1..-O3 produced wrong results for a later tile of this warp, -O0 did not)
+          double x0, x1, q0, q1;
+          tgj_x<RT>(acc[jj], P, wv, x0, x1);
+          tgj_update<RT>(acc[jj], x0, x1, sh.M[s]);
+          tgj_pick<RT>(acc[jj], nx, q0, q1);
+          TGJ_TR(192 + nx);
+          const TgjPivot pv = tgj_invert(q0, q1, nc);
+          TGJ_TR(208 + nx);
           mbar_wait(&sh.empty[s1], ((uint32_t(pc + 1) / NB) & 1u) ^ 1u);
-          const int nc = nx == NP - 1 ? ncl : 8;
-          const bool live_col = g < nc;
+          sh.W[s1][tgj_slot(2 * t, g)] = sh.Wall[nx][tgj_slot(2 * t, g)] = pv.w0;
+          sh.W[s1][tgj_slot(2 * t + 1, g)] = sh.Wall[nx][tgj_slot(2 * t + 1, g)] = pv.w1;
+          sh.L[s1][tgj_slot(2 * t, g)] = pv.l0;
+          sh.L[s1][tgj_slot(2 * t + 1, g)] = pv.l1;
 #pragma unroll
           for (int i = 0; i < RT; ++i) {
             sh.M[s1][i][tgj_slot(2 * t, g)] = live_col ? -acc[jj][i][0] : 0.0;
@@ -415,15 +499,10 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
           }
           sh.M[s1][nx][tgj_slot(2 * t, g)] = 0.0;  // the pivot row tile is left unscaled
           sh.M[s1][nx][tgj_slot(2 * t + 1, g)] = 0.0;
-          sh.W[s1][tgj_slot(2 * t, g)] = sh.Wall[nx][tgj_slot(2 * t, g)] = pv.w0;
-          sh.W[s1][tgj_slot(2 * t + 1, g)] = sh.Wall[nx][tgj_slot(2 * t + 1, g)] = pv.w1;
-          sh.L[s1][tgj_slot(2 * t, g)] = pv.l0;
-          sh.L[s1][tgj_slot(2 * t + 1, g)] = pv.l1;
           __syncwarp();
-          if (lane == 0) {
-            if (pv.bad) sh.fail = 1;
-            mbar_arrive(&sh.full[s1]);
-          }
+          if (lane == 0 && pv.bad) sh.fail = 1;
+          TGJ_TR(224 + nx);
+          if (lane == 0) mbar_arrive(&sh.full[s1]);
         }
         if (pend >= 0) {
           finish_panel(pend, jn);
@@ -442,6 +521,7 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
       }
     }
     pc0 += NP;
+    TGJ_TR(240 + warp);
 
     // ---- δ = W_i y_i per row tile from the unscaled column N; stop rule; status ----
     __syncthreads();
@@ -499,6 +579,7 @@ __global__ void __launch_bounds__(NW * 32, 2) newton_tgj_kernel(const NewtonPara
     }
     if (p.hint_out)  // the row order used (identity): the next iteration's hint
       for (int k = tid; k < N; k += NT) p.hint_out[int64_t(b) * N + k] = int16_t(k);
+    TGJ_TR(250);
     __syncthreads();  // shared state (rhs, red, Wall, fail) is rewritten by the next sample
   }
 }
