@@ -12,7 +12,12 @@
  *   rbns_solve               <- online.solve_block, batched ("batch sweep API")
  *   rbns_solve_host          <- same, host buffers in/out (the query API a CPU caller binds)
  *   rbns_reduced_operator    <- online.reduced_operator (residual + Jacobian)
+ *   rbns_solve_ex            <- same as rbns_solve with this call's statistics returned through an out-parameter
+ *                               (per-query phase timings, "timing instrumentation is
+ *                               per-query and contention-free")
  *   rbns_recover_pressure    <- solve_block step 2, B_sp p = f_s - A_sv u
+ *   rbns_reconstruct_pressure<- online.reconstruct_pressure, combined scheme: p = P_att u with the model's
+ *                               attached pressure modes
  *   rbns_error_string        <- errors.RbflowError messages (reference errors.py:4-21)
  *
  * All arrays are IEEE fp64 (or the stated integer type), row-major, C-contiguous.  "dev" pointers are CUDA
@@ -30,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RBNS_ABI_VERSION 2
+#define RBNS_ABI_VERSION 3
 #define RBNS_MAX_TERMS 256 /* per term family */
 #define RBNS_MAX_GROUPS 4  /* distinct mu1 powers tying linear terms to the quadratic blocks (see create2) */
 
@@ -59,7 +64,8 @@ enum rbns_error {
   RBNS_ERR_CUDA = 2,
   RBNS_ERR_OUT_OF_MEMORY = 3,
   RBNS_ERR_UNSUPPORTED = 4,
-  RBNS_ERR_NO_PRESSURE = 5
+  RBNS_ERR_NO_PRESSURE = 5,
+  RBNS_ERR_NO_ATTACHED = 6     /* reconstruct_pressure on a model without attached pressure modes */
 };
 
 typedef struct rbns_theta_term {
@@ -117,11 +123,18 @@ typedef struct rbns_model_desc2 {
   rbns_term_family load;       /* count x N                                              */
   rbns_term_family coupling;   /* count x Np x N        (Np > 0)                         */
   const double* Mp;            /* host Np x Np SPD, or NULL when Np = 0                  */
+  /* ABI 3: optional attached pressure modes of the combined scheme ("optional attached pressure
+   * modes for the combined scheme"): column j holds the pressure data attached to velocity mode j, so the
+   * reconstructed pressure is p = P_att u.  n_att = 0 / P_att = NULL: none. */
+  int32_t n_att;               /* rows of P_att (pressure coefficients)                 */
+  int32_t reserved2;
+  const double* P_att;         /* host n_att x N                                         */
 } rbns_model_desc2;
 
 typedef struct rbns_model rbns_model;
 
-/* Per-call statistics of the last rbns_solve / rbns_solve_host on this model (thread-unsafe read). */
+/* Statistics of one solve: returned per call by rbns_solve_ex / rbns_solve_host_ex; rbns_get_stats reads the
+ * most recent call's copy kept on the model (a convenience for single-threaded callers). */
 typedef struct rbns_stats {
   int64_t sample_iterations;      /* sum over samples of Newton iterations performed               */
   int64_t contraction_iterations; /* sample-iterations that ran the convective GEMM (iter >= 2)    */
@@ -164,11 +177,21 @@ int64_t rbns_model_device_bytes(const rbns_model* model);
 int rbns_solve(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter,
                double* u, double* p, int32_t* iters, int8_t* status, double* last_update, void* stream);
 
+/* rbns_solve with this call's statistics written to *stats (may be NULL): concurrent solves on different
+ * streams each get their own numbers. */
+int rbns_solve_ex(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter, double* u,
+                  double* p, int32_t* iters, int8_t* status, double* last_update, rbns_stats* stats, void* stream);
+
 /* Same as rbns_solve with HOST buffers: the call copies mu in and results out (the end-to-end path a
  * CPU-side caller binds; host<->device copies are part of the call). */
 int rbns_solve_host(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter,
                     double* u, double* p, int32_t* iters, int8_t* status, double* last_update,
                     void* stream);
+
+/* rbns_solve_host with per-call statistics (see rbns_solve_ex). */
+int rbns_solve_host_ex(rbns_model* model, const double* mu, int64_t batch, double tol, int32_t max_iter, double* u,
+                       double* p, int32_t* iters, int8_t* status, double* last_update, rbns_stats* stats,
+                       void* stream);
 
 /* Residual and Jacobian of the reduced system at states eta, batched (debug / FD tests).
  *   mu dev B x 2, eta dev B x N, residual dev B x N, jacobian dev B x N x N (row l, column m = dR_l/du_m) */
@@ -179,6 +202,12 @@ int rbns_reduced_operator(rbns_model* model, const double* mu, const double* eta
  * status (dev, may be NULL) receives RBNS_SINGULAR_RECOVERY where Mp could not be factored. */
 int rbns_recover_pressure(rbns_model* model, const double* mu, const double* u, int64_t batch,
                           double* p, int8_t* status, void* stream);
+
+/* Combined-scheme pressure reconstruction: p = P_att u for every sample, device buffers.
+ *   u dev B x N, p dev B x n_att.  RBNS_ERR_NO_ATTACHED when the model carries no attached modes. */
+int rbns_reconstruct_pressure(rbns_model* model, const double* u, int64_t batch, double* p, void* stream);
+/* rows of P_att (0: none) */
+int rbns_model_attached(const rbns_model* model, int32_t* n_att);
 
 int rbns_get_stats(const rbns_model* model, rbns_stats* out);
 

@@ -22,10 +22,13 @@ STATUS_NAMES = {0: "CONVERGED", 1: "NON_CONVERGED", 2: "SINGULAR_SYSTEM", 3: "SI
 
 # every symbol include/rbns.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (
-    "rbns_model_create", "rbns_model_create2", "rbns_model_terms", "rbns_model_destroy", "rbns_model_info", "rbns_model_device_bytes", "rbns_solve",
-    "rbns_solve_host", "rbns_reduced_operator", "rbns_recover_pressure", "rbns_get_stats",
-    "rbns_error_string", "rbns_last_error_message", "rbns_abi_version",
+    "rbns_model_create", "rbns_model_create2", "rbns_model_terms", "rbns_model_destroy", "rbns_model_info",
+    "rbns_model_device_bytes", "rbns_model_attached", "rbns_solve", "rbns_solve_ex", "rbns_solve_host",
+    "rbns_solve_host_ex", "rbns_reduced_operator", "rbns_recover_pressure", "rbns_reconstruct_pressure",
+    "rbns_get_stats", "rbns_error_string", "rbns_last_error_message", "rbns_abi_version",
 )
+ABI_VERSION = 3
+ERR_NO_ATTACHED = 6
 
 
 class ThetaTermC(ctypes.Structure):
@@ -48,7 +51,8 @@ class TermFamilyC(ctypes.Structure):
 class ModelDesc2C(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("n_p", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("n_stop", ctypes.c_int32), ("linear", TermFamilyC), ("quadratic", TermFamilyC),
-                ("load", TermFamilyC), ("coupling", TermFamilyC), ("Mp", ctypes.c_void_p)]
+                ("load", TermFamilyC), ("coupling", TermFamilyC), ("Mp", ctypes.c_void_p),
+                ("n_att", ctypes.c_int32), ("reserved2", ctypes.c_int32), ("P_att", ctypes.c_void_p)]
 
 
 class StatsC(ctypes.Structure):
@@ -90,6 +94,11 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     solve_args = [vp, vp, i64, dbl, i32, vp, vp, vp, vp, vp, vp]
     lib.rbns_solve.argtypes = solve_args
     lib.rbns_solve_host.argtypes = solve_args
+    solve_ex_args = [vp, vp, i64, dbl, i32, vp, vp, vp, vp, vp, ctypes.POINTER(StatsC), vp]
+    lib.rbns_solve_ex.argtypes = solve_ex_args
+    lib.rbns_solve_host_ex.argtypes = solve_ex_args
+    lib.rbns_reconstruct_pressure.argtypes = [vp, vp, i64, vp, vp]
+    lib.rbns_model_attached.argtypes = [vp, ctypes.POINTER(i32)]
     lib.rbns_reduced_operator.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     lib.rbns_recover_pressure.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     lib.rbns_get_stats.argtypes = [vp, ctypes.POINTER(StatsC)]
@@ -98,6 +107,9 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.rbns_last_error_message.argtypes = []
     lib.rbns_last_error_message.restype = ctypes.c_char_p
     lib.rbns_abi_version.restype = ctypes.c_int
+    if lib.rbns_abi_version() != ABI_VERSION:
+        raise NativeError(f"{p}: ABI version {lib.rbns_abi_version()}, this package binds {ABI_VERSION} "
+                          "(rebuild with __graft_entry__.build())")
     for name in EXPORTED_SYMBOLS:
         if name not in ("rbns_model_device_bytes", "rbns_error_string", "rbns_last_error_message",
                         "rbns_abi_version"):

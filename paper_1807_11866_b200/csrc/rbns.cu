@@ -133,7 +133,9 @@ struct rbns_model {
   int nu_lin = 0;
   int jl = 0;                              // J block layout the Newton kernels read (jidx)
   int n_stop = 0, stop_abs = 0;            // stop norm over the leading n_stop unknowns; absolute or relative
-  Operand vel, prs;
+  Operand vel, prs, att;                   // velocity contraction, pressure coupling, attached pressure modes
+  int n_att = 0;                           // rows of P_att (combined-scheme reconstruction), 0 = none
+  cudaMemPool_t pool = nullptr;            // private stream-ordered pool of the per-call workspaces
   double* f = nullptr;                     // [Qf][N]
   double* L = nullptr;                     // [Np][Np]
   double* Lt = nullptr;                    // [Np][Np]
@@ -277,15 +279,17 @@ struct Timer {
   }
 };
 
-// Per-call workspace: stream-ordered allocations and events, released on every exit path.
+// Per-call workspace: stream-ordered allocations from the handle's private pool (kept pooled between calls,
+// released with the handle; the device's default pool is never touched) and events, freed on every exit path.
 struct SolveWorkspace {
   cudaStream_t st;
+  cudaMemPool_t pool;
   std::vector<void*> bufs;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
-  explicit SolveWorkspace(cudaStream_t s) : st(s) {}
+  SolveWorkspace(cudaStream_t s, cudaMemPool_t p) : st(s), pool(p) {}
   template <class T>
   cudaError_t alloc(T** p, size_t bytes) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, st);
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
     if (e == cudaSuccess) bufs.push_back(*p);
     return e;
   }
@@ -303,7 +307,7 @@ int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double*
   const int64_t budget = env_int64("RBNS_RBUF_BYTES", int64_t(1) << 30);
   const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldr * 8)));
   double* rbuf = nullptr;
-  SolveWorkspace ws(st);
+  SolveWorkspace ws(st, m->pool);
   RBNS_CUDA(ws.alloc(&rbuf, size_t(cap) * ldr * sizeof(double)));
   const int cp = (m->Np + 31) / 32;
   int rc = RBNS_OK;
@@ -334,11 +338,31 @@ int recover(rbns_model* m, const double* mu, const double* u, int64_t B, double*
   return rc;
 }
 
+// Combined-scheme reconstruction p = P_att u: the contraction kernel with the one-block operand S = P_att
+// (θ ≡ 1) into a tile-padded buffer, then the n_att leading columns of each row into p.
+int reconstruct(rbns_model* m, const double* u, int64_t B, double* p, cudaStream_t st) {
+  const int64_t ldr = m->att.row_tiles * kBN;
+  const int64_t budget = env_int64("RBNS_RBUF_BYTES", int64_t(1) << 30);
+  const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldr * 8)));
+  double* rbuf = nullptr;
+  SolveWorkspace ws(st, m->pool);
+  RBNS_CUDA(ws.alloc(&rbuf, size_t(cap) * ldr * sizeof(double)));
+  int rc = RBNS_OK;
+  for (int64_t c0 = 0; c0 < B && rc == RBNS_OK; c0 += cap) {
+    const int nc = int(std::min<int64_t>(cap, B - c0));
+    rc = launch_contract(m, m->att, nullptr, nc, u + c0 * m->N, nullptr, rbuf, ldr, st);
+    if (rc) break;
+    copy_leading<<<grid_for(int64_t(nc) * m->n_att, 256), 256, 0, st>>>(rbuf, ldr, nc, m->n_att, p + c0 * m->n_att);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(RBNS_ERR_CUDA, "copy_leading launch failed");
+  }
+  return rc;
+}
+
 int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
-                 int32_t* iters, int8_t* status, double* last, cudaStream_t st) {
+                 int32_t* iters, int8_t* status, double* last, cudaStream_t st, rbns_stats* stats_out) {
   rbns_stats stats{};
   Timer timer(st);
-  SolveWorkspace ws(st);
+  SolveWorkspace ws(st, m->pool);
   RBNS_CUDA(cudaEventCreate(&ws.t0));
   RBNS_CUDA(cudaEventCreate(&ws.t1));
   RBNS_CUDA(cudaEventRecord(ws.t0, st));
@@ -455,6 +479,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
     stats.ms_recovery = timer.total(2);
     stats.ms_assembly = timer.total(3);
     stats.pivot_fallbacks = hcount[1];
+    if (stats_out) *stats_out = stats;
     std::lock_guard<std::mutex> lk(m->stats_mu);
     m->stats = stats;
   }
@@ -488,6 +513,7 @@ const char* rbns_error_string(int code) {
     case RBNS_ERR_OUT_OF_MEMORY: return "out of device memory";
     case RBNS_ERR_UNSUPPORTED: return "unsupported configuration";
     case RBNS_ERR_NO_PRESSURE: return "model has no pressure-recovery operators";
+    case RBNS_ERR_NO_ATTACHED: return "model has no attached pressure modes";
     default: return "unknown error";
   }
 }
@@ -566,6 +592,8 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   if (d->n_p > 0 && (!d->Mp || d->coupling.count < 1))
     return fail(RBNS_ERR_INVALID_ARGUMENT, "Np > 0 needs Mp and >= 1 coupling term");
   if (d->n_p > 256) return fail(RBNS_ERR_UNSUPPORTED, "Np > 256");
+  if (d->n_att < 0 || (d->n_att > 0 && !d->P_att))
+    return fail(RBNS_ERR_INVALID_ARGUMENT, "attached pressure modes: n_att < 0 or NULL P_att");
   if (!newton_supported(d->n))
     return fail(RBNS_ERR_UNSUPPORTED, "N=" + std::to_string(d->n) + " exceeds the register-resident Newton kernel");
   int ndev = 0;
@@ -645,8 +673,9 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
     return op.smem <= size_t(max_smem);
   };
   const int Qb = int(blocks.size());
+  m->n_att = d->n_att > 0 ? d->n_att : 0;
   if (!plan(m->vel, int64_t(m->N) * m->N + int64_t(m->G) * m->N, Qb, Qa) ||
-      (m->Np && !plan(m->prs, m->Np, m->Qp, 0)))
+      (m->Np && !plan(m->prs, m->Np, m->Qp, 0)) || (m->n_att && !plan(m->att, m->n_att, 1, 0)))
     return cleanup(fail(RBNS_ERR_UNSUPPORTED, "contraction tile does not fit shared memory for N=" +
                                                   std::to_string(m->N)));
   // a per-function cap shared by every model: set it to the device maximum (not this model's size), so a
@@ -655,11 +684,17 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
     return cleanup(fail(RBNS_ERR_CUDA, "cudaFuncSetAttribute(contract) failed"));
   if (newton_prepare(m->N) != cudaSuccess) return cleanup(fail(RBNS_ERR_CUDA, "Newton kernel attributes failed"));
 
-  // keep freed stream-ordered allocations pooled (no re-allocation between calls)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+  // private stream-ordered pool for the per-call workspaces: allocations stay pooled between calls (no
+  // re-allocation on the hot path) and are returned to the device when the handle is destroyed
+  {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&m->pool, &props) != cudaSuccess)
+      return cleanup(fail(RBNS_ERR_CUDA, "cudaMemPoolCreate failed"));
     uint64_t thr = ~0ULL;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(m->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
 
   auto step = [&](cudaError_t e, const char* what) {
@@ -678,6 +713,8 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   th.insert(th.end(), d->linear.theta, d->linear.theta + Qa);
   if (m->Qf) th.insert(th.end(), d->load.theta, d->load.theta + m->Qf);
   if (m->Qp) th.insert(th.end(), d->coupling.theta, d->coupling.theta + m->Qp);
+  const rbns_theta_term one{RBNS_THETA_CONST, 0, 0, 0, 1.0};
+  if (d->n_att > 0) th.push_back(one);  // the attached-mode operand: one block, θ ≡ 1
   if (!step(cudaMalloc(&m->dth, th.size() * sizeof(rbns_theta_term)), "cudaMalloc(theta)") ||
       !step(cudaMemcpy(m->dth, th.data(), th.size() * sizeof(rbns_theta_term), cudaMemcpyHostToDevice),
             "upload theta"))
@@ -686,6 +723,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   m->vel.thl = m->dth + Qb;
   m->thf = m->dth + Qb + Qa;
   m->prs.thb = m->dth + Qb + Qa + m->Qf;
+  m->att.thb = m->dth + Qb + Qa + m->Qf + m->Qp;
 
   const int64_t N = m->N;
   double *dC = nullptr, *dA = nullptr, *drho = nullptr;
@@ -750,6 +788,22 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
     if (rc) return cleanup(rc);
     m->bytes += np * m->prs.kalloc * 8 + 2 * np * np * 8;
   }
+  if (m->n_att) {  // attached pressure modes: S_att[i][k] = P_att[i][k] (one block, θ ≡ 1)
+    const int64_t na = m->n_att;
+    double* dPa = nullptr;
+    ok = step(cudaMalloc(&dPa, size_t(na) * N * sizeof(double)), "cudaMalloc(P_att)") &&
+         step(cudaMemcpy(dPa, d->P_att, size_t(na) * N * sizeof(double), cudaMemcpyHostToDevice), "upload P_att") &&
+         step(cudaMalloc(&m->att.S, size_t(na) * m->att.kalloc * sizeof(double)), "cudaMalloc(Satt)");
+    if (ok) {
+      build_pressure_operator<<<m->num_sms, 256>>>(m->att.S, m->n_att, m->att.kalloc, dPa, m->N, m->Ne, 1);
+      ok = step(cudaGetLastError(), "build attached operator") && step(cudaDeviceSynchronize(), "build Satt");
+    }
+    if (dPa) cudaFree(dPa);
+    if (!ok) return bad();
+    rc = make_tensor_map(&m->att.tm, m->att.S, m->n_att, m->att.kalloc);
+    if (rc) return cleanup(rc);
+    m->bytes += na * m->att.kalloc * 8;
+  }
   *out = m;
   return RBNS_OK;
 }
@@ -757,9 +811,11 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
 int rbns_model_destroy(rbns_model* m) {
   if (!m) return RBNS_OK;
   DeviceGuard guard(m->device);
-  for (void* p : {static_cast<void*>(m->vel.S), static_cast<void*>(m->prs.S), static_cast<void*>(m->f),
-                  static_cast<void*>(m->L), static_cast<void*>(m->Lt), static_cast<void*>(m->dth)})
+  for (void* p : {static_cast<void*>(m->vel.S), static_cast<void*>(m->prs.S), static_cast<void*>(m->att.S),
+                  static_cast<void*>(m->f), static_cast<void*>(m->L), static_cast<void*>(m->Lt),
+                  static_cast<void*>(m->dth)})
     if (p) cudaFree(p);
+  if (m->pool) cudaMemPoolDestroy(m->pool);  // every call has synchronized and freed its workspace
   delete m;
   return RBNS_OK;
 }
@@ -793,21 +849,28 @@ int rbns_get_stats(const rbns_model* m, rbns_stats* out) {
   return RBNS_OK;
 }
 
-int rbns_solve(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
-               int32_t* iters, int8_t* status, double* last, void* stream) {
+int rbns_solve_ex(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
+                  int32_t* iters, int8_t* status, double* last, rbns_stats* stats, void* stream) {
   int rc = check_solve_args(m, mu, B, tol, max_iter, u, iters, status, last);
   if (rc) return rc;
   if (p && !m->Np) return fail(RBNS_ERR_NO_PRESSURE, "pressure output requested but model has no Mp/Bq");
+  if (stats) *stats = rbns_stats{};
   if (B == 0) return RBNS_OK;
   DeviceGuard guard(m->device);
-  return solve_device(m, mu, B, tol, max_iter, u, p, iters, status, last, static_cast<cudaStream_t>(stream));
+  return solve_device(m, mu, B, tol, max_iter, u, p, iters, status, last, static_cast<cudaStream_t>(stream), stats);
 }
 
-int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
-                    int32_t* iters, int8_t* status, double* last, void* stream) {
+int rbns_solve(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
+               int32_t* iters, int8_t* status, double* last, void* stream) {
+  return rbns_solve_ex(m, mu, B, tol, max_iter, u, p, iters, status, last, nullptr, stream);
+}
+
+int rbns_solve_host_ex(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u,
+                       double* p, int32_t* iters, int8_t* status, double* last, rbns_stats* stats, void* stream) {
   int rc = check_solve_args(m, mu, B, tol, max_iter, u, iters, status, last);
   if (rc) return rc;
   if (p && !m->Np) return fail(RBNS_ERR_NO_PRESSURE, "pressure output requested but model has no Mp/Bq");
+  if (stats) *stats = rbns_stats{};
   if (B == 0) return RBNS_OK;
   DeviceGuard guard(m->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -815,7 +878,7 @@ int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int3
   int32_t* di = nullptr;
   int8_t* ds = nullptr;
   const size_t N = m->N, np = m->Np;
-  SolveWorkspace ws(st);
+  SolveWorkspace ws(st, m->pool);
   RBNS_CUDA(ws.alloc(&dmu, B * 2 * sizeof(double)));
   RBNS_CUDA(ws.alloc(&du, B * N * sizeof(double)));
   if (p) RBNS_CUDA(ws.alloc(&dp, B * np * sizeof(double)));
@@ -823,7 +886,7 @@ int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int3
   RBNS_CUDA(ws.alloc(&di, B * sizeof(int32_t)));
   RBNS_CUDA(ws.alloc(&ds, B * sizeof(int8_t)));
   RBNS_CUDA(cudaMemcpyAsync(dmu, mu, B * 2 * sizeof(double), cudaMemcpyHostToDevice, st));
-  rc = solve_device(m, dmu, B, tol, max_iter, du, dp, di, ds, dl, st);
+  rc = solve_device(m, dmu, B, tol, max_iter, du, dp, di, ds, dl, st, stats);
   if (rc == RBNS_OK) {
     RBNS_CUDA(cudaMemcpyAsync(u, du, B * N * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (p) RBNS_CUDA(cudaMemcpyAsync(p, dp, B * np * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -836,28 +899,59 @@ int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int3
   return rc;
 }
 
+int rbns_solve_host(rbns_model* m, const double* mu, int64_t B, double tol, int32_t max_iter, double* u, double* p,
+                    int32_t* iters, int8_t* status, double* last, void* stream) {
+  return rbns_solve_host_ex(m, mu, B, tol, max_iter, u, p, iters, status, last, nullptr, stream);
+}
+
 int rbns_reduced_operator(rbns_model* m, const double* mu, const double* eta, int64_t B, double* residual,
                           double* jacobian, void* stream) {
   if (!m || B < 0 || (B > 0 && (!mu || !eta || !residual || !jacobian)))
     return fail(RBNS_ERR_INVALID_ARGUMENT, "bad arguments to rbns_reduced_operator");
+  if (B > (int64_t(1) << 31) - 1) return fail(RBNS_ERR_INVALID_ARGUMENT, "batch out of range");
   if (B == 0) return RBNS_OK;
   DeviceGuard guard(m->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t ldy = m->vel.row_tiles * kBN;
+  const int64_t budget = env_int64("RBNS_JBUF_BYTES", int64_t(8) << 30);
+  const int64_t cap = std::max<int64_t>(kBM, std::min<int64_t>(B, budget / (ldy * 8)));
   double* y = nullptr;
-  SolveWorkspace ws(st);
-  RBNS_CUDA(ws.alloc(&y, size_t(B) * ldy * sizeof(double)));
-  int rc = launch_contract(m, m->vel, nullptr, int(B), eta, mu, y, ldy, st);
-  if (rc == RBNS_OK) {
+  SolveWorkspace ws(st, m->pool);
+  RBNS_CUDA(ws.alloc(&y, size_t(cap) * ldy * sizeof(double)));
+  const int64_t N = m->N;
+  int rc = RBNS_OK;
+  for (int64_t c0 = 0; c0 < B && rc == RBNS_OK; c0 += cap) {  // chunks of the Y buffer
+    const int nc = int(std::min<int64_t>(cap, B - c0));
+    rc = launch_contract(m, m->vel, nullptr, nc, eta + c0 * N, mu + 2 * c0, y, ldy, st);
+    if (rc) break;
     NewtonParams np = newton_params(m);
-    np.n = int32_t(B);
-    np.mu = mu;
-    operator_readout<<<int(B), 128, 0, st>>>(y, ldy, eta, np, residual, jacobian);
+    np.n = nc;
+    np.mu = mu + 2 * c0;
+    operator_readout<<<nc, 128, 0, st>>>(y, ldy, eta + c0 * N, np, residual + c0 * N, jacobian + c0 * N * N);
     if (cudaGetLastError() != cudaSuccess) rc = fail(RBNS_ERR_CUDA, "operator_readout launch failed");
   }
   cudaError_t se = cudaStreamSynchronize(st);
   if (rc == RBNS_OK && se != cudaSuccess) rc = fail(RBNS_ERR_CUDA, std::string("reduced_operator: ") + cudaGetErrorString(se));
   return rc;
+}
+
+int rbns_reconstruct_pressure(rbns_model* m, const double* u, int64_t B, double* p, void* stream) {
+  if (!m || B < 0 || (B > 0 && (!u || !p))) return fail(RBNS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (!m->n_att) return fail(RBNS_ERR_NO_ATTACHED, "model carries no attached pressure modes (combined scheme)");
+  if (B > (int64_t(1) << 31) - 1) return fail(RBNS_ERR_INVALID_ARGUMENT, "batch out of range");
+  if (B == 0) return RBNS_OK;
+  DeviceGuard guard(m->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = reconstruct(m, u, B, p, st);
+  cudaError_t se = cudaStreamSynchronize(st);
+  if (rc == RBNS_OK && se != cudaSuccess) rc = fail(RBNS_ERR_CUDA, std::string("reconstruct: ") + cudaGetErrorString(se));
+  return rc;
+}
+
+int rbns_model_attached(const rbns_model* m, int32_t* n_att) {
+  if (!m || !n_att) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL argument");
+  *n_att = m->n_att;
+  return RBNS_OK;
 }
 
 int rbns_recover_pressure(rbns_model* m, const double* mu, const double* u, int64_t B, double* p, int8_t* status,

@@ -65,6 +65,14 @@ __global__ void build_pressure_operator(double* __restrict__ S, int np, int kall
   }
 }
 
+// out[b][i] = y[b][i], i < cols (the leading columns of a tile-padded contraction output)
+__global__ void copy_leading(const double* __restrict__ y, int64_t ldy, int32_t n, int32_t cols, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(n) * cols; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = e / cols;
+    out[e] = y[b * ldy + (e - b * cols)];
+  }
+}
+
 __global__ void init_solve(int32_t* act, int8_t* status, int32_t* iters, double* last, int64_t B) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < B; i += int64_t(gridDim.x) * blockDim.x) {
     act[i] = int32_t(i);

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = w[q];
         for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = w[p.Qb + q];
       } else {
-        const double mu0 = p.mu[2 * id], mu1 = p.mu[2 * id + 1];
+        const double mu0 = p.mu ? p.mu[2 * id] : 0.0, mu1 = p.mu ? p.mu[2 * id + 1] : 1.0;  // NULL: μ-free operand
         const double nu = p.nu_lin ? 1.0 / mu1 : 1.0;
         for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = eval_theta(p.thb[q], mu0, mu1);
         for (int q = 0; q < p.Ql; ++q) thnuS[q * BM + b] = nu * eval_theta(p.thl[q], mu0, mu1);

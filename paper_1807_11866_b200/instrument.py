@@ -1,7 +1,9 @@
 """Quadrature-evaluation counter (mirror of /root/reference/pkg/src/rbflow/instrument.py:1-17).
 
-The online solvers of this package never perform quadrature; tests assert that this counter (and, in the
-development container, the reference's own counter) is unchanged across online calls.
+The offline projection (projection.py) counts its quadrature points here; the online solvers never perform
+quadrature, and the tests assert that this counter is unchanged across every online call while a projection
+call does increment it, and — where the reference package is importable — that the reference's
+own counter is unchanged by the package's host-side online code.
 """
 
 QUADRATURE_EVALS = 0

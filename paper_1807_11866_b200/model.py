@@ -14,6 +14,9 @@ families (``AffineFormSet``) as they enter the reduced residual
 * ``f``  (Qf, N)       load family: projected loads and the lift's d0 terms (u∞¹ and u∞² families);
 * ``Bq`` (Qb, Np, N) + SPD ``Mp`` (Np, Np): optional pressure recovery M_p p = Σ_b θ_b(μ) B_b u
                         (BASELINE.json config 4; the role of B_sp).
+* ``P_att`` (n_att, N): optional attached pressure modes of the combined scheme ("optional attached
+                        pressure modes for the combined scheme"): column j is the pressure data
+                        attached to velocity mode j, so reconstruction is p = P_att u.
 
 Descriptors: ``theta`` is the shared list of the BASELINE configs (one θ per term index for every family);
 the ``theta_*`` fields override it per family (the paper's models: a-terms ν·φᵏ, c-terms φᵏ, c0-terms u∞·φᵏ,
@@ -52,6 +55,7 @@ class ReducedModel:
     nu_linear: bool = True
     n_stop: int = 0                    # leading unknowns in the Newton stop norm (0: all N)
     stop_absolute: bool = False        # ‖δ‖ ≤ tol (coupled rule) instead of ‖δ‖ ≤ tol·‖u‖
+    P_att: Optional[np.ndarray] = None # (n_att, N)    attached pressure modes (combined scheme), or None
 
     def __post_init__(self):
         A = np.ascontiguousarray(self.A, dtype=np.float64)
@@ -75,6 +79,12 @@ class ReducedModel:
                 raise ValueError(f"inconsistent pressure shapes Mp{Mp.shape} Bq{Bq.shape}")
             object.__setattr__(self, "Mp", Mp)
             object.__setattr__(self, "Bq", Bq)
+        if self.P_att is not None:
+            P_att = np.ascontiguousarray(self.P_att, dtype=np.float64)
+            if P_att.ndim != 2 or P_att.shape[1] != n or P_att.shape[0] < 1:
+                raise ValueError(f"attached pressure modes P_att{P_att.shape} must be (n_att >= 1, {n})")
+            P_att.flags.writeable = False
+            object.__setattr__(self, "P_att", P_att)
         counts = {"linear": A.shape[0], "quadratic": C.shape[0], "load": f.shape[0],
                   "coupling": 0 if self.Bq is None else self.Bq.shape[0]}
         for fam in FAMILIES:
@@ -111,6 +121,11 @@ class ReducedModel:
     @property
     def n_p(self) -> int:
         return 0 if self.Mp is None else self.Mp.shape[0]
+
+    @property
+    def n_att(self) -> int:
+        """Rows of the attached pressure modes (0: the model carries none)."""
+        return 0 if self.P_att is None else self.P_att.shape[0]
 
     @property
     def stop_dim(self) -> int:

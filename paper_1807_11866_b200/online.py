@@ -12,7 +12,9 @@ Public API (names and meaning follow the SPEC):
   SINGULAR_SYSTEM / SINGULAR_RECOVERY (SPEC.md:514, :524); NON_CONVERGED is reported, not raised.
 * :func:`solve_block_batch` (rm, μ[B,2]) → :class:`BatchSolution` — the batch sweep API.
 * :func:`reduced_operator` (rm, μ, η) → (residual, Jacobian) — SPEC.md:500-508.
-* :func:`reconstruct_pressure` — recovery alone for given velocities (SPEC.md:523 step 2).
+* :func:`recover_pressure` — a-posteriori recovery alone for given velocities (SPEC.md:523 step 2).
+* :func:`reconstruct_pressure` (rm, u_coeffs) → p_coeffs — the combined scheme's reconstruction from the
+  model's attached pressure modes, p = P_att u.
 * :func:`sweep_report` — the batch sweep's tabular (CSV) report.
 * :class:`DeviceModel` — the uploaded, immutable operator handle (one per device), for callers that keep
   tensors on the GPU.
@@ -29,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .errors import NativeError, SingularSystemError
+from .errors import NativeError, RbflowError, SingularSystemError
 from .model import ReducedModel
 
 CONVERGED, NON_CONVERGED, SINGULAR_SYSTEM, SINGULAR_RECOVERY, NONFINITE = 0, 1, 2, 3, 4
@@ -94,6 +96,8 @@ def _native_desc(model: ReducedModel):
         fam.data = data.ctypes.data if data is not None else None
         fam.theta = arr
     desc.Mp = model.Mp.ctypes.data if model.Mp is not None else None
+    desc.n_att = model.n_att
+    desc.P_att = model.P_att.ctypes.data if model.P_att is not None else None
     return desc, keep
 
 
@@ -142,6 +146,10 @@ class DeviceModel:
     def n_p(self) -> int:
         return self.model.n_p
 
+    @property
+    def n_att(self) -> int:
+        return self.model.n_att
+
     def terms(self) -> dict:
         """Term plan of the device handle: family sizes, contraction blocks, h groups (rbns_model_terms)."""
         c = (ctypes.c_int32 * 6)()
@@ -152,9 +160,45 @@ class DeviceModel:
         return int(self.lib.rbns_model_device_bytes(self._h))
 
     def stats(self) -> dict:
+        """Statistics of the most recent solve on this handle (per-call numbers are in BatchSolution.stats)."""
         st = _native.StatsC()
         _native.check(self.lib.rbns_get_stats(self._h, ctypes.byref(st)), "rbns_get_stats")
         return st.as_dict()
+
+    def _check_out(self, out: BatchSolution, b: int, want_p: bool) -> None:
+        """A caller-supplied ``out`` must hold the batch: shapes, dtypes, this device, contiguous; p when
+        pressure is requested (the kernels write every row, so a short or strided buffer would be overrun)."""
+        specs = (("u", out.u, (self.n,), torch.float64), ("iters", out.iters, (), torch.int32),
+                 ("status", out.status, (), torch.int8), ("last_update", out.last_update, (), torch.float64))
+        if want_p:
+            if out.p is None:
+                raise ValueError("pressure requested but out.p is None")
+            specs += (("p", out.p, (self.n_p,), torch.float64),)
+        for name, t, tail, dt in specs:
+            if not isinstance(t, torch.Tensor):
+                raise ValueError(f"out.{name} must be a torch tensor")
+            if t.dim() != 1 + len(tail) or t.shape[0] < b or tuple(t.shape[1:]) != tail:
+                raise ValueError(f"out.{name} has shape {tuple(t.shape)}, need ({b}+{''.join(', ' + str(x) for x in tail)})")
+            if t.dtype != dt:
+                raise ValueError(f"out.{name} has dtype {t.dtype}, need {dt}")
+            if t.device != self.device:
+                raise ValueError(f"out.{name} is on {t.device}, the model is on {self.device}")
+            if not t.is_contiguous():
+                raise ValueError(f"out.{name} must be contiguous")
+
+    def _check_host_out(self, out: dict, b: int, want_p: bool) -> None:
+        specs = (("u", (self.n,), np.float64), ("iters", (), np.int32), ("status", (), np.int8),
+                 ("last_update", (), np.float64))
+        if want_p:
+            specs += (("p", (self.n_p,), np.float64),)
+        for name, tail, dt in specs:
+            a = out.get(name)
+            if not isinstance(a, np.ndarray):
+                raise ValueError(f"out[{name!r}] must be a numpy array")
+            if a.ndim != 1 + len(tail) or a.shape[0] < b or tuple(a.shape[1:]) != tail or a.dtype != dt:
+                raise ValueError(f"out[{name!r}] is {a.dtype}{a.shape}, need {np.dtype(dt)}({b}, ...{tail})")
+            if not a.flags.c_contiguous:
+                raise ValueError(f"out[{name!r}] must be C-contiguous")
 
     # -- device-buffer API ------------------------------------------------------------------------------
     def _mu_tensor(self, mu) -> torch.Tensor:
@@ -179,11 +223,14 @@ class DeviceModel:
                 iters=torch.empty(b, dtype=torch.int32, **kw),
                 status=torch.empty(b, dtype=torch.int8, **kw),
                 last_update=torch.empty(b, dtype=torch.float64, **kw))
-        rc = self.lib.rbns_solve(self._h, mu.data_ptr(), b, float(tol), int(max_iter), out.u.data_ptr(),
-                                 _ptr(out.p) if want_p else None, out.iters.data_ptr(), out.status.data_ptr(),
-                                 out.last_update.data_ptr(), _stream_handle(stream, self.device))
-        _native.check(rc, "rbns_solve")
-        out.stats = self.stats()
+        else:
+            self._check_out(out, b, want_p)
+        st = _native.StatsC()
+        rc = self.lib.rbns_solve_ex(self._h, mu.data_ptr(), b, float(tol), int(max_iter), out.u.data_ptr(),
+                                    _ptr(out.p) if want_p else None, out.iters.data_ptr(), out.status.data_ptr(),
+                                    out.last_update.data_ptr(), ctypes.byref(st), _stream_handle(stream, self.device))
+        _native.check(rc, "rbns_solve_ex")
+        out.stats = st.as_dict()
         return out
 
     def solve_host(self, mu: np.ndarray, tol: float = DEFAULT_TOL, max_iter: int = DEFAULT_MAX_ITER,
@@ -197,12 +244,16 @@ class DeviceModel:
             out = dict(u=np.empty((b, self.n)), p=np.empty((b, self.n_p)) if want_p else None,
                        iters=np.empty(b, dtype=np.int32), status=np.empty(b, dtype=np.int8),
                        last_update=np.empty(b))
-        rc = self.lib.rbns_solve_host(self._h, mu.ctypes.data, b, float(tol), int(max_iter),
-                                      out["u"].ctypes.data, out["p"].ctypes.data if want_p else None,
-                                      out["iters"].ctypes.data, out["status"].ctypes.data,
-                                      out["last_update"].ctypes.data, _stream_handle(stream, self.device))
-        _native.check(rc, "rbns_solve_host")
-        out["stats"] = self.stats()
+        else:
+            self._check_host_out(out, b, want_p)
+        st = _native.StatsC()
+        rc = self.lib.rbns_solve_host_ex(self._h, mu.ctypes.data, b, float(tol), int(max_iter),
+                                         out["u"].ctypes.data, out["p"].ctypes.data if want_p else None,
+                                         out["iters"].ctypes.data, out["status"].ctypes.data,
+                                         out["last_update"].ctypes.data, ctypes.byref(st),
+                                         _stream_handle(stream, self.device))
+        _native.check(rc, "rbns_solve_host_ex")
+        out["stats"] = st.as_dict()
         return out
 
     def reduced_operator(self, mu, eta, stream=None) -> Tuple[torch.Tensor, torch.Tensor]:
@@ -227,6 +278,20 @@ class DeviceModel:
                       "rbns_recover_pressure")
         return p, st
 
+    def reconstruct_pressure(self, u, stream=None) -> torch.Tensor:
+        """Combined-scheme reconstruction p = P_att u (rbns_reconstruct_pressure)."""
+        if not self.n_att:
+            raise RbflowError("reconstruct_pressure: the reduced model carries no attached pressure modes "
+                              "(combined scheme, SPEC.md:530-538)")
+        u = torch.as_tensor(u, dtype=torch.float64).to(self.device)
+        u = u.reshape(-1, self.n).contiguous()
+        b = u.shape[0]
+        p = torch.empty((b, self.n_att), dtype=torch.float64, device=self.device)
+        _native.check(self.lib.rbns_reconstruct_pressure(self._h, u.data_ptr(), b, p.data_ptr(),
+                                                         _stream_handle(stream, self.device)),
+                      "rbns_reconstruct_pressure")
+        return p
+
 
 # ---- model-level convenience API (SPEC names) ------------------------------------------------------------
 
@@ -249,15 +314,72 @@ def release_device_models() -> None:
     _cache.clear()
 
 
+def _phase_times(stats: dict) -> Dict[str, float]:
+    """SPEC phase timings (seconds) from one call's device statistics: assembly = the u = 0 affine assembly plus
+    the contraction launches (θ-weighted assembly of J fused with the convective contraction), solve = the
+    Newton-update kernels, recovery = pressure recovery / reconstruction."""
+    return {"assembly": (stats.get("ms_assembly", 0.0) + stats.get("ms_gemm", 0.0)) * 1e-3,
+            "solve": stats.get("ms_lu", 0.0) * 1e-3, "recovery": stats.get("ms_recovery", 0.0) * 1e-3}
+
+
+def _merge_stats(parts) -> dict:
+    out = {}
+    for st in parts:
+        for k, v in st.items():
+            if k.startswith("ms_") or k == "newton_rounds":
+                out[k] = max(out.get(k, 0), v)  # devices run concurrently: wall-clock phase = slowest device
+            else:
+                out[k] = out.get(k, 0) + v
+    return out
+
+
 def solve_block_batch(rm: ReducedModel, mus, tol: float = DEFAULT_TOL, max_iter: int = DEFAULT_MAX_ITER,
-                      pressure: bool = True, device: int = 0) -> BatchSolution:
-    """Batch sweep over μ samples on the GPU; returns device tensors."""
-    return device_model(rm, device).solve(mus, tol=tol, max_iter=max_iter, pressure=pressure)
+                      pressure: bool | str = True, device: int = 0, devices=None) -> BatchSolution:
+    """Batch sweep over μ samples on the GPU; returns device tensors.
+
+    ``pressure``: True / "recovery" (the block solver's a-posteriori recovery), "combined" (the
+    combined scheme: velocity solve, then p = P_att u from the attached modes), False / "none".
+    ``devices``: several GPUs (μ-sharded, one host thread and one model handle per device, no collective;
+    SURVEY.md §8(e)); the result is gathered on ``devices[0]``.  Per-sample results are bit-identical to a
+    single-device solve (each sample's arithmetic is independent of the batch it is in)."""
+    mode = {True: "recovery", False: "none", None: "none"}.get(pressure, pressure)
+    if mode not in ("recovery", "combined", "none"):
+        raise ValueError(f"pressure={pressure!r}: use 'recovery', 'combined' or 'none'")
+    devs = list(devices) if devices else [device]
+    mus_t = torch.as_tensor(mus, dtype=torch.float64).reshape(-1, 2)
+
+    def run(dev, mu_part):
+        dm = device_model(rm, dev)
+        sol = dm.solve(mu_part.to(dm.device), tol=tol, max_iter=max_iter, pressure=mode == "recovery")
+        if mode == "combined":
+            stream = torch.cuda.current_stream(dm.device)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sol.p = dm.reconstruct_pressure(sol.u, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            sol.stats["ms_recovery"] = e0.elapsed_time(e1)
+        return sol
+
+    if len(devs) == 1:
+        return run(devs[0], mus_t)
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .sharding import shard_bounds
+
+    bounds = [shard_bounds(mus_t.shape[0], len(devs), r) for r in range(len(devs))]
+    with ThreadPoolExecutor(len(devs)) as ex:  # ctypes releases the GIL during every library call
+        parts = list(ex.map(lambda i: run(devs[i], mus_t[bounds[i][0]:bounds[i][1]]), range(len(devs))))
+    home = torch.device("cuda", devs[0])
+    cat = lambda name: torch.cat([getattr(s, name).to(home) for s in parts])  # noqa: E731  (NVLink peer copies)
+    return BatchSolution(u=cat("u"), p=None if parts[0].p is None else cat("p"), iters=cat("iters"),
+                         status=cat("status"), last_update=cat("last_update"),
+                         stats=_merge_stats([s.stats for s in parts]))
 
 
 def solve_block(rm: ReducedModel, mu, tol: float = DEFAULT_TOL, max_iter: int = DEFAULT_MAX_ITER,
                 device: int = 0) -> ReducedSolution:
-    """Single query.  s = 0 exactly; phase timings from the device events."""
+    """Single query.  s = 0 exactly; phase timings from the device events of this call."""
     dm = device_model(rm, device)
     mu_np = np.asarray(mu, dtype=np.float64).reshape(2)
     t0 = time.perf_counter()
@@ -268,13 +390,12 @@ def solve_block(rm: ReducedModel, mu, tol: float = DEFAULT_TOL, max_iter: int = 
         raise SingularSystemError(f"SINGULAR_SYSTEM at mu={tuple(mu_np)} after {int(res['iters'][0])} iterations")
     if st == SINGULAR_RECOVERY:
         raise SingularSystemError(f"SINGULAR_RECOVERY at mu={tuple(mu_np)}: pressure Gramian not SPD")
-    s = res["stats"]
+    wt = _phase_times(res["stats"])
+    wt["total"] = wall
     return ReducedSolution(
         mu=(float(mu_np[0]), float(mu_np[1])), u_coeffs=res["u"][0].copy(), s_coeffs=np.zeros(rm.n),
         p_coeffs=None if res["p"] is None else res["p"][0].copy(), newton_iters=int(res["iters"][0]),
-        wall_time={"assembly": s["ms_gemm"] * 1e-3, "solve": s["ms_lu"] * 1e-3,
-                   "recovery": s["ms_recovery"] * 1e-3, "total": wall},
-        converged=st == CONVERGED, status=st, last_update=float(res["last_update"][0]))
+        wall_time=wt, converged=st == CONVERGED, status=st, last_update=float(res["last_update"][0]))
 
 
 def reduced_operator(rm: ReducedModel, mu, eta, device: int = 0) -> Tuple[np.ndarray, np.ndarray]:
@@ -283,10 +404,26 @@ def reduced_operator(rm: ReducedModel, mu, eta, device: int = 0) -> Tuple[np.nda
     return r[0].cpu().numpy(), j[0].cpu().numpy()
 
 
-def reconstruct_pressure(rm: ReducedModel, mus, u, device: int = 0) -> torch.Tensor:
-    """Pressure recovery for given velocity coefficients."""
+def recover_pressure(rm: ReducedModel, mus, u, device: int = 0) -> torch.Tensor:
+    """A-posteriori pressure recovery for given velocity coefficients: B_sp p = f_s − A_sv u (SPEC.md:523,
+    PAPER.md:905-908); the config-4 form M_p p = Σ_q θ_q(μ) B_q u."""
     p, _ = device_model(rm, device).recover_pressure(mus, u)
     return p
+
+
+def reconstruct_pressure(rm: ReducedModel, u_coeffs, device: int = 0):
+    """p_coeffs = u_coeffs applied to the model's attached pressure modes (combined scheme,
+    PAPER.md:941-986), p = P_att u, on the device.  One state (N,) gives (n_att,) numpy; a batch (B, N) gives
+    (B, n_att) — numpy for numpy input, a device tensor for tensor input.  Raises RbflowError when the model
+    carries no attached modes ("errors: rm lacks attached modes")."""
+    if rm.P_att is None:
+        raise RbflowError("reconstruct_pressure: the reduced model carries no attached pressure modes "
+                          "(built without the combined flag, SPEC.md:449)")
+    p = device_model(rm, device).reconstruct_pressure(u_coeffs)
+    if isinstance(u_coeffs, torch.Tensor):
+        return p if u_coeffs.dim() > 1 else p[0]
+    out = p.cpu().numpy()
+    return out if np.ndim(u_coeffs) > 1 else out[0]
 
 
 SWEEP_COLUMNS = ("phi", "u_inf", "solver", "iters", "status", "last_update", "converged",
@@ -306,7 +443,7 @@ def sweep_report(mus, sol: BatchSolution, path=None, solver: str = "block") -> s
     st = sol.status.cpu().numpy()
     last = sol.last_update.cpu().numpy()
     b = max(1, len(mus))
-    per = {k: sol.stats.get(f"ms_{k}", 0.0) * 1e-3 / b for k in ("gemm", "lu", "recovery")}
+    per = {k: v / b for k, v in _phase_times(sol.stats).items()}
     buf = io.StringIO()
     w = csv.writer(buf, lineterminator="\n")
     buf.write("# rbflow batch sweep report v1\n")
@@ -315,7 +452,7 @@ def sweep_report(mus, sol: BatchSolution, path=None, solver: str = "block") -> s
              SINGULAR_RECOVERY: "SINGULAR_RECOVERY", NONFINITE: "NONFINITE"}
     for i in range(len(mus)):
         w.writerow([repr(float(mus[i, 0])), repr(float(mus[i, 1])), solver, int(it[i]), names.get(int(st[i]), int(st[i])),
-                    repr(float(last[i])), int(st[i]) == CONVERGED, repr(per["gemm"]), repr(per["lu"]),
+                    repr(float(last[i])), int(st[i]) == CONVERGED, repr(per["assembly"]), repr(per["solve"]),
                     repr(per["recovery"])])
     text = buf.getvalue()
     if path is not None:

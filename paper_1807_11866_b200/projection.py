@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import torch
 
+from . import instrument
 from .errors import NativeError
 
 
@@ -42,6 +43,7 @@ def project_convection(val_u, grad, val_w, w, device="cuda", chunk_bytes: int = 
     if g.shape != (p_tot, 2, 2, n) or vw.shape != (p_tot, 2, n) or wt.shape != (p_tot,):
         raise ValueError(f"tabulation shapes val_u{tuple(vu.shape)} grad{tuple(g.shape)} val_w{tuple(vw.shape)} "
                          f"w{tuple(wt.shape)}")
+    instrument.count_quadrature(p_tot)  # offline quadrature (the online stage must never do this)
     step = max(1, chunk_bytes // (2 * n * n * 8))
     out = torch.zeros((n, n * n), dtype=torch.float64, device=device)       # [l, (j,k)]
     for p0 in range(0, p_tot, step):
@@ -56,6 +58,7 @@ def project_viscous(grad, w, nu: float = 1.0, device="cuda") -> torch.Tensor:
     """A (N, N) = ν Σ_p w_p Σ_{c,d} grad[p,c,d,j] grad[p,c,d,k] (one DGEMM)."""
     g, wt = _dev(grad, device), _dev(w, device)
     p_tot, _, _, n = g.shape
+    instrument.count_quadrature(p_tot)
     G = (torch.sqrt(wt)[:, None, None, None] * g).reshape(-1, n) if bool((wt >= 0).all()) else None
     if G is None:
         raise ValueError("negative quadrature weights")
@@ -65,4 +68,5 @@ def project_viscous(grad, w, nu: float = 1.0, device="cuda") -> torch.Tensor:
 def project_load(val_w, w, force, device="cuda") -> torch.Tensor:
     """f (N,) = Σ_p w_p Σ_c force[p,c] val_w[p,c,j] for a body force tabulated at the quadrature points."""
     vw, wt, fo = _dev(val_w, device), _dev(w, device), _dev(force, device)
+    instrument.count_quadrature(wt.shape[0])
     return torch.einsum("p,pc,pcj->j", wt, fo, vw)

@@ -74,6 +74,8 @@ def save_model(model: ReducedModel, path: os.PathLike) -> Path:
     if model.Mp is not None:
         arrays["Mp"] = model.Mp
         arrays["Bq"] = model.Bq
+    if model.P_att is not None:  # attached pressure modes of the combined scheme
+        arrays["P_att"] = model.P_att
     families = {}
     for fam in FAMILIES:
         if fam == "coupling" and model.Bq is None:
@@ -89,7 +91,7 @@ def save_model(model: ReducedModel, path: os.PathLike) -> Path:
     manifest = {
         "format": FORMAT, "version": VERSION, "name": model.name,
         "kind": "velocity-only block (div-conforming, Piola)" if not model.shared_theta else "velocity-only block",
-        "basis": {"n_velocity": model.n, "n_pressure": model.n_p},
+        "basis": {"n_velocity": model.n, "n_pressure": model.n_p, "n_attached_pressure": model.n_att},
         "viscosity": "nu = 1/mu1 multiplies the linear family" if model.nu_linear else "in the descriptors",
         "nu_linear": model.nu_linear,
         "stop": {"n_stop": model.n_stop, "absolute": model.stop_absolute},
@@ -154,6 +156,7 @@ def load_model(path: os.PathLike, mmap: bool = False) -> ReducedModel:
                             name=man.get("name", "reduced-model"), meta=dict(man.get("provenance", {})),
                             theta_linear=thetas["linear"], theta_quadratic=thetas["quadratic"],
                             theta_load=thetas["load"], theta_coupling=thetas.get("coupling"), nu_linear=nu_linear,
-                            n_stop=int(stop["n_stop"]), stop_absolute=bool(stop["absolute"]))
+                            n_stop=int(stop["n_stop"]), stop_absolute=bool(stop["absolute"]),
+                            P_att=arrays.get("P_att"))
     except (KeyError, ValueError) as exc:
         raise StoreError(f"{path}: arrays inconsistent with the families ({exc})") from exc

@@ -51,7 +51,10 @@ CONFIGS = {
 
 
 def make_model(n: int, q: int, theta_family: str, n_p: int = 0, seed: int = 0,
-               kappa_c: float = 1e-5, name: str = "synthetic") -> ReducedModel:
+               kappa_c: float = 1e-5, name: str = "synthetic", attached: int = 0) -> ReducedModel:
+    """BASELINE.json generators (SURVEY.md Appendix B pins).  ``attached`` > 0 adds combined-scheme attached
+    pressure modes P_att (attached × n, N(0,1)/√n), drawn after every other array so the other operators are
+    unchanged."""
     rng = np.random.default_rng(seed)
     A = np.empty((q, n, n))
     G = rng.standard_normal((n, n))
@@ -68,8 +71,9 @@ def make_model(n: int, q: int, theta_family: str, n_p: int = 0, seed: int = 0,
         H = rng.standard_normal((n_p, n_p))
         Mp = H @ H.T / n_p + np.eye(n_p)
         Bq = rng.standard_normal((q, n_p, n)) / np.sqrt(n)
-    return ReducedModel(A=A, C=C, f=f, theta=family(theta_family), Mp=Mp, Bq=Bq, name=name,
-                        meta={"seed": seed, "kappa_c": kappa_c, "family": theta_family})
+    P_att = rng.standard_normal((attached, n)) / np.sqrt(n) if attached else None
+    return ReducedModel(A=A, C=C, f=f, theta=family(theta_family), Mp=Mp, Bq=Bq, name=name, P_att=P_att,
+                        meta={"seed": seed, "kappa_c": kappa_c, "family": theta_family, "attached": attached})
 
 
 def make_mu(batch: int, re_max: float, seed: int = 1, re_min: float = 10.0,
@@ -81,9 +85,11 @@ def make_mu(batch: int, re_max: float, seed: int = 1, re_min: float = 10.0,
     return np.ascontiguousarray(np.stack([alpha, re], axis=1))
 
 
-def config_model(cfg: Config | int) -> ReducedModel:
+def config_model(cfg: Config | int, attached: bool = False) -> ReducedModel:
+    """The config's model; ``attached`` adds n_p (or N) combined-scheme attached pressure modes."""
     cfg = CONFIGS[cfg] if isinstance(cfg, int) else cfg
-    return make_model(cfg.n, cfg.q, cfg.theta_family, n_p=cfg.n_p, kappa_c=cfg.kappa_c, name=cfg.name)
+    return make_model(cfg.n, cfg.q, cfg.theta_family, n_p=cfg.n_p, kappa_c=cfg.kappa_c, name=cfg.name,
+                      attached=(cfg.n_p or cfg.n) if attached else 0)
 
 
 def config_mu(cfg: Config | int, batch: int | None = None) -> np.ndarray:

@@ -37,7 +37,7 @@ def test_all_header_symbols_exported(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rbns_abi_version() == 2
+    assert lib.rbns_abi_version() == 3
     assert lib.rbns_error_string(0) == b"ok"
     assert b"invalid" in lib.rbns_error_string(1)
     assert lib.rbns_error_string(99) == b"unknown error"
@@ -79,11 +79,34 @@ def test_missing_library_fails_loudly(tmp_path):
         _native.load(tmp_path / "librbns.so")
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of the header structs: sizes and every field offset, checked against the C compiler."""
+    import shutil
+    import subprocess
+
     from paper_1807_11866_b200 import _native
 
-    assert ctypes.sizeof(_native.ThetaTermC) == 24
-    assert ctypes.sizeof(_native.ModelDescC) == 16 + 6 * 8
-    assert ctypes.sizeof(_native.TermFamilyC) == 24
-    assert ctypes.sizeof(_native.ModelDesc2C) == 16 + 4 * 24 + 8
-    assert ctypes.sizeof(_native.StatsC) == 16 + 16 + 40 + 8
+    structs = {"rbns_theta_term": _native.ThetaTermC, "rbns_model_desc": _native.ModelDescC,
+               "rbns_term_family": _native.TermFamilyC, "rbns_model_desc2": _native.ModelDesc2C,
+               "rbns_stats": _native.StatsC}
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "rbns.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run([cc, f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        c, f, v = ln.split()
+        got[(c, f)] = int(v)
+    for cname, cls in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, f"{cname}.{fname}"

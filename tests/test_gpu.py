@@ -324,12 +324,145 @@ def test_monomial_family_and_single_query(dms):
 
 
 def test_zero_quadrature_online(cfg_model, dms):
-    """The online path performs no quadrature (instrument.py:3-5)."""
-    from paper_1807_11866_b200 import instrument
+    """The online path performs no quadrature (reference instrument.py:3-5): the package's counter,
+    which the offline projection increments (checked, so the probe is live), is unchanged across every online
+    entry point, and the online path never imports the reference's quadrature assembly."""
+    import sys
 
+    from paper_1807_11866_b200 import instrument, projection
+
+    rng = np.random.default_rng(0)
     before = instrument.quadrature_evals()
-    device_solve(dms(0, cfg_model(0)), synthetic.config_mu(0))
+    projection.project_viscous(rng.standard_normal((12, 2, 2, 4)), np.full(12, 0.5))
+    assert instrument.quadrature_evals() == before + 12  # the probe counts offline quadrature
+    before = instrument.quadrature_evals()
+    model = synthetic.config_model(4, attached=True)
+    mu = synthetic.config_mu(4, 64)
+    with online.DeviceModel(model, 0) as dm:
+        sol = dm.solve(torch.from_numpy(mu).cuda())
+        dm.recover_pressure(mu, sol.u)
+        dm.reconstruct_pressure(sol.u)
+        dm.reduced_operator(mu[:4], sol.u[:4])
+    online.solve_block(cfg_model(0), synthetic.config_mu(0)[0])
+    online.sweep_report(synthetic.config_mu(0), online.solve_block_batch(cfg_model(0), synthetic.config_mu(0)))
+    torch.cuda.synchronize()
     assert instrument.quadrature_evals() == before
+    assert not any(m == "rbflow" or m.startswith("rbflow.") for m in sys.modules)
+
+
+# ---- combined scheme: pressure reconstruction from attached modes (SPEC.md:530-538) -----------------------
+
+def test_reconstruct_pressure_parity_and_kats():
+    """p = P_att u on the device against the oracle; u = 0 → p = 0 and linearity exactly."""
+    model = synthetic.config_model(4, attached=True)
+    mu = synthetic.config_mu(4, 1024)
+    ur, _, _, _ = oracle.solve_batch(model, mu)
+    with online.DeviceModel(model, 0) as dm:
+        p = dm.reconstruct_pressure(torch.from_numpy(ur).cuda()).cpu().numpy()
+        z = dm.reconstruct_pressure(torch.zeros((8, model.n), dtype=torch.float64)).cpu().numpy()
+        p2 = dm.reconstruct_pressure(torch.from_numpy(2.0 * ur).cuda()).cpu().numpy()
+    pr = oracle.reconstruct_pressure(model, ur)
+    assert rel_err(p, pr) <= 1e-13
+    assert np.all(z == 0.0)
+    assert np.array_equal(p2, 2.0 * p)  # exact: scaling by 2 is exact in every product and sum
+    # SPEC surface: one state in, one pressure vector out; batched numpy in, numpy out
+    one = online.reconstruct_pressure(model, ur[3])
+    assert one.shape == (model.n_att,) and rel_err(one, pr[3]) <= 1e-13
+    online.release_device_models()
+
+
+def test_reconstruct_pressure_requires_attached_modes(cfg_model):
+    from paper_1807_11866_b200.errors import RbflowError
+
+    with pytest.raises(RbflowError, match="attached"):
+        online.reconstruct_pressure(cfg_model(4), np.zeros(100))
+    with online.DeviceModel(cfg_model(4), 0) as dm:
+        with pytest.raises(RbflowError):
+            dm.reconstruct_pressure(np.zeros((2, 100)))
+        lib = dm.lib
+        rc = lib.rbns_reconstruct_pressure(dm._h, 0, 0, 0, None)
+        assert rc == 6  # RBNS_ERR_NO_ATTACHED through the raw C ABI
+
+
+def test_combined_scheme_batch_and_timing():
+    """solve_block_batch(pressure="combined") = velocity solve + reconstruction; the reconstruction is no
+    slower than the recovery solve it replaces ("combined-reconstruction ≤ block time")."""
+    model = synthetic.config_model(4, attached=True)
+    mu = synthetic.config_mu(4, 16384)
+    rec = online.solve_block_batch(model, mu, pressure="recovery")
+    comb = online.solve_block_batch(model, mu, pressure="combined")
+    torch.cuda.synchronize()
+    assert torch.equal(rec.u, comb.u) and torch.equal(rec.iters, comb.iters)
+    pr = oracle.reconstruct_pressure(model, comb.u.cpu().numpy())
+    assert rel_err(comb.p.cpu().numpy(), pr) <= 1e-13
+    t_rec = min(online.solve_block_batch(model, mu, pressure="recovery").stats["ms_recovery"] for _ in range(3))
+    t_comb = min(online.solve_block_batch(model, mu, pressure="combined").stats["ms_recovery"] for _ in range(3))
+    assert t_comb <= t_rec, (t_comb, t_rec)
+    online.release_device_models()
+
+
+# ---- boundary hygiene --------------------------------------------------------------------------------------
+
+def test_out_buffers_are_validated(cfg_model, dms):
+    dm = dms(4, cfg_model(4))
+    mu = torch.from_numpy(synthetic.config_mu(4, 64)).cuda()
+    good = dm.solve(mu)
+    small = dm.solve(mu[:32])
+    with pytest.raises(ValueError, match="shape"):
+        dm.solve(mu, out=small)                               # too few rows
+    bad = online.BatchSolution(u=good.u, p=None, iters=good.iters, status=good.status, last_update=good.last_update)
+    with pytest.raises(ValueError, match="pressure"):
+        dm.solve(mu, out=bad)                                  # p requested, none given
+    bad = online.BatchSolution(u=good.u.float(), p=good.p, iters=good.iters, status=good.status,
+                               last_update=good.last_update)
+    with pytest.raises(ValueError, match="dtype"):
+        dm.solve(mu, out=bad)
+    bad = online.BatchSolution(u=good.u.cpu(), p=good.p, iters=good.iters, status=good.status,
+                               last_update=good.last_update)
+    with pytest.raises(ValueError, match="cuda|device|on"):
+        dm.solve(mu, out=bad)
+    wide = torch.empty((64, 2 * dm.n), dtype=torch.float64, device="cuda")
+    bad = online.BatchSolution(u=wide[:, ::2], p=good.p, iters=good.iters, status=good.status,
+                               last_update=good.last_update)
+    with pytest.raises(ValueError):
+        dm.solve(mu, out=bad)                                  # strided view
+    host = dm.solve_host(mu.cpu().numpy())
+    host["u"] = host["u"][:10]
+    with pytest.raises(ValueError):
+        dm.solve_host(mu.cpu().numpy(), out=host)
+    again = dm.solve(mu, out=good)                             # a valid buffer is reused
+    assert again.u.data_ptr() == good.u.data_ptr()
+
+
+def test_per_call_stats_and_phase_times(cfg_model, dms):
+    """Statistics come back per call (rbns_solve_ex), so two calls of different sizes report their own work;
+    solve_block's assembly phase includes the u = 0 affine assembly."""
+    dm = dms(1, cfg_model(1))
+    mu = torch.from_numpy(synthetic.config_mu(1, 512)).cuda()
+    a = dm.solve(mu[:64])
+    b = dm.solve(mu)
+    assert a.stats["sample_iterations"] == int(a.iters.sum()) and b.stats["sample_iterations"] == int(b.iters.sum())
+    assert dm.stats()["sample_iterations"] == b.stats["sample_iterations"]  # the handle keeps the latest copy
+    sol = online.solve_block(cfg_model(1), synthetic.config_mu(1, 1)[0])
+    s = online.device_model(cfg_model(1)).stats()
+    assert sol.wall_time["assembly"] == pytest.approx((s["ms_assembly"] + s["ms_gemm"]) * 1e-3)
+    assert s["ms_assembly"] > 0.0
+
+
+def test_multi_device_batch_is_bitwise_single_device(cfg_model):
+    """solve_block_batch(devices=[...]): μ-sharded, one handle and host thread per device, gathered on the first
+    device — bit-identical to one device (two handles on one B200 stand in for two GPUs)."""
+    model = cfg_model(4)
+    mu = synthetic.config_mu(4, 3001)
+    one = online.solve_block_batch(model, mu)
+    torch.cuda.synchronize()
+    u1, p1, it1 = one.u.clone(), one.p.clone(), one.iters.clone()
+    ndev = max(2, torch.cuda.device_count())
+    two = online.solve_block_batch(model, mu, devices=[i % torch.cuda.device_count() for i in range(ndev)])
+    torch.cuda.synchronize()
+    assert torch.equal(two.u, u1) and torch.equal(two.p, p1) and torch.equal(two.iters, it1)
+    assert two.stats["sample_iterations"] == int(it1.sum())
+    online.release_device_models()
 
 
 def test_concurrent_streams(cfg_model, dms):
@@ -346,6 +479,7 @@ def test_concurrent_streams(cfg_model, dms):
         b = dm.solve(mu[256:], stream=s2)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([a.u, b.u]), ref_u)
+    assert a.stats["sample_iterations"] == int(a.iters.sum()) and b.stats["sample_iterations"] == int(b.iters.sum())
 
 
 @pytest.mark.parametrize("n", [40, 100, 150])

@@ -68,3 +68,29 @@ def test_sweep_report_is_deterministic(tmp_path):
     lines = t1.strip().split("\n")
     assert lines[0].startswith("#") and lines[1].split(",") == list(online.SWEEP_COLUMNS)
     assert len(lines) == 2 + 3 and "NON_CONVERGED" in lines[4] and lines[2].split(",")[3] == "4"
+
+
+def test_reference_quadrature_counter_untouched_by_host_online_code(tmp_path):
+    """Where the reference package is importable (this development container), the package's host-side online
+    code — model construction, the store round trip, the C-ABI descriptor packing, report formatting — leaves the
+    reference's own quadrature counter (rbflow/instrument.py:8-17) unchanged; the device side is
+    covered by tests/test_gpu.py::test_zero_quadrature_online."""
+    import sys
+    from pathlib import Path
+
+    src = Path("/root/reference/pkg/src")
+    if not src.is_dir():
+        pytest.skip("reference package not present (GPU box)")
+    sys.path.insert(0, str(src))
+    try:
+        from rbflow import instrument as ref_instrument
+    finally:
+        sys.path.remove(str(src))
+    from paper_1807_11866_b200 import online, store
+
+    before = ref_instrument.quadrature_evals()
+    m = synthetic.make_model(12, 3, "trig3", n_p=4, attached=4)
+    back = store.load_model(store.save_model(m, tmp_path / "m.rbm"))
+    desc, _ = online._native_desc(back)
+    assert desc.n == 12 and desc.n_att == 4
+    assert ref_instrument.quadrature_evals() == before

@@ -37,7 +37,7 @@ def test_manifest_contents(tmp_path):
     m = synthetic.make_lifted_model(6, 1)
     p = store.save_model(m, tmp_path / "m.rbm")
     man = json.loads((p / "manifest.json").read_text())
-    assert man["format"] == "rbflow-reduced-model" and man["basis"] == {"n_velocity": 6, "n_pressure": 0}
+    assert man["format"] == "rbflow-reduced-model" and man["basis"] == {"n_velocity": 6, "n_pressure": 0, "n_attached_pressure": 0}
     assert set(man["families"]) == {"linear", "quadratic", "load"}
     assert len(man["families"]["linear"]["terms"]) == 4 * 1 + 3 + 4 * 1 + 1
     assert man["arrays"]["C"]["shape"] == [5, 6, 6, 6]
@@ -80,3 +80,19 @@ def test_store_to_device(tmp_path):
         r1, r2 = d1.solve(mu), d2.solve(mu)
         torch.cuda.synchronize()
         assert torch.equal(r1.u, r2.u) and torch.equal(r1.p, r2.p) and torch.equal(r1.iters, r2.iters)
+
+
+def test_attached_pressure_modes_round_trip(tmp_path):
+    """The combined scheme's attached pressure modes are stored and hashed with the model."""
+    m = synthetic.make_model(8, 3, "trig3", n_p=5, attached=5)
+    p = store.save_model(m, tmp_path / "att.rbm")
+    back = store.load_model(p)
+    assert back.n_att == 5
+    np.testing.assert_array_equal(back.P_att, m.P_att)
+    man = json.loads((p / "manifest.json").read_text())
+    assert man["basis"]["n_attached_pressure"] == 5 and "P_att" in man["arrays"]
+    raw = bytearray((p / "P_att.f64").read_bytes())
+    raw[0] ^= 1
+    (p / "P_att.f64").write_bytes(bytes(raw))
+    with pytest.raises(store.StoreError):
+        store.load_model(p)
