@@ -1,15 +1,17 @@
-// rbns_newton.cu — instantiation + dispatch of the register-resident Gauss–Jordan Newton-update kernel
-// (rbns_newton.cuh); kept in its own translation unit so the instantiations compile in parallel with the rest
-// of the library.  A few fixed shapes cover every N ≤ 127 (RS·TGR ≥ N rows, CS·TGC ≥ N+1 columns).
+// rbns_newton.cu — instantiation + dispatch of the Newton-update kernels; kept in its own translation unit so
+// the instantiations compile in parallel with the rest of the library.
+//   tiled Gauss–Jordan (rbns_tgj.cuh)      default where a shape is instantiated (N = 49..55, 89..103)
+//   speculative rank-1 (rbns_newton_spec)   other N ≤ 127, hinted pivot order, misses → exact kernel
+//   exact rank-1 (rbns_newton2.cuh)         full partial-pivot search: every miss of the speculative kernels
+//   2-CTA cluster (rbns_newton_cluster)     127 < N ≤ 207
+// RBNS_NEWTON=gjs forces the speculative rank-1 kernels, RBNS_NEWTON=gj2 the exact one (parity-tested).
 #include "rbns_launch.h"
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
-#include "rbns_bgj.cuh"
 #include "rbns_newton.cuh"
 #include "rbns_newton2.cuh"
-#include "rbns_newton3.cuh"
 #include "rbns_newton_spec.cuh"
 #include "rbns_newton_cluster.cuh"
 #include "rbns_tgj.cuh"
@@ -44,43 +46,12 @@ const Shape kShapes2[] = {
     {8, 16, 13, 7, newton_gj2_kernel<8, 16, 13, 7>},
     {16, 16, 8, 8, newton_gj2_kernel<16, 16, 8, 8>},
 };
-// RBNS_NEWTON=gj1: the earlier owner-serial pivot search (rbns_newton.cuh), kept for comparison
-const Shape kShapes1[] = {
-    {4, 8, 4, 3, newton_gj_kernel<4, 8, 4, 3>},
-    {4, 8, 8, 5, newton_gj_kernel<4, 8, 8, 5>},
-    {4, 8, 13, 7, newton_gj_kernel<4, 8, 13, 7>},
-    {8, 16, 10, 6, newton_gj_kernel<8, 16, 10, 6>},
-    {8, 16, 13, 7, newton_gj_kernel<8, 16, 13, 7>},
-    {16, 16, 8, 8, newton_gj_kernel<16, 16, 8, 8>},
-};
-
-// RBNS_NEWTON=gj3: one barrier per step, redundant per-warp search, pivot row by warp shuffles (rbns_newton3.cuh)
-const Shape kShapes3[] = {
-    {4, 8, 4, 3, newton_gj3_kernel<4, 8, 4, 3>},
-    {4, 8, 8, 5, newton_gj3_kernel<4, 8, 8, 5>},
-    {4, 8, 13, 7, newton_gj3_kernel<4, 8, 13, 7>},
-    {8, 16, 10, 6, newton_gj3_kernel<8, 16, 10, 6>},
-    {8, 16, 13, 7, newton_gj3_kernel<8, 16, 13, 7>},
-    {16, 16, 8, 8, newton_gj3_kernel<16, 16, 8, 8>},
-};
-
-// RBNS_GJ_WIDE=1: 8 warps (16×16 grid, 49 register doubles per thread, two CTAs per SM) for 52 < N ≤ 112
-const Shape kWide = {16, 16, 7, 7, newton_gj_kernel<16, 16, 7, 7>};
-
 const Shape* plan(int N) {
-  static const bool wide = [] {
-    const char* v = std::getenv("RBNS_GJ_WIDE");
-    return v && v[0] == '1';
-  }();
-  if (wide && N > 52 && N <= 111) return &kWide;
-  static const int variant = [] {
+  static const bool full_search = [] {  // RBNS_NEWTON=gj2: the exact kernel for every sample
     const char* v = std::getenv("RBNS_NEWTON");
-    if (v && std::strcmp(v, "gj1") == 0) return 1;
-    if (v && std::strcmp(v, "gj3") == 0) return 3;
-    if (v && std::strcmp(v, "gj2") == 0) return 2;
-    return 0;
+    return v && std::strcmp(v, "gj2") == 0;
   }();
-  const Shape* table = variant == 1 ? kShapes1 : variant == 2 ? kShapes2 : variant == 3 ? kShapes3 : kShapes;
+  const Shape* table = full_search ? kShapes2 : kShapes;
   for (int i = 0; i < int(sizeof(kShapes) / sizeof(kShapes[0])); ++i) {
     const Shape& s = table[i];
     if (N >= 1 && N <= s.tgr * s.rs && N + 1 <= s.tgc * s.cs) return &s;
@@ -88,52 +59,20 @@ const Shape* plan(int N) {
   return nullptr;
 }
 
-// blocked (DMMA) variant: RT×CT tiles of 8×8, NW warps
-struct BShape {
-  int rt, ct, nw;
-  NewtonKernel kern;
-  size_t smem;
-};
-
-#define RBNS_BS(R_, C_, W_) {R_, C_, W_, newton_bgj_kernel<R_, C_, W_>, sizeof(BGJShared<R_, C_, W_>)}
-const BShape kBShapes[] = {
-    RBNS_BS(2, 2, 2),     // N ≤ 15
-    RBNS_BS(7, 7, 4),     // N ≤ 55
-    RBNS_BS(12, 12, 4),   // N ≤ 95
-    {13, 13, 4, newton_bgj_kernel<13, 13, 4, 1>, sizeof(BGJShared<13, 13, 4>)},  // N ≤ 103 (tile 0 never in
-                                                                                  // registers: 4 warps, 2 CTAs/SM)
-    RBNS_BS(16, 16, 8),   // N ≤ 127
-};
-#undef RBNS_BS
-
-const BShape* bplan(int N) {
-  for (const BShape& s : kBShapes)
-    if (N >= 1 && N <= 8 * s.rt && N + 1 <= 8 * s.ct) return &s;
-  return nullptr;
-}
-
-// Kernel choice: the blocked DMMA kernel (rbns_bgj.cuh) is the default where it measured faster (88 < N ≤ 103:
-// cfg-2 Newton update 74 ms against 89 ms for the speculative rank-1 kernel); elsewhere the rank-1 register
-// kernels (rbns_newton*.cuh) run.  RBNS_NEWTON=bgj forces the blocked kernel for every N it covers, any other
-// RBNS_NEWTON value forces the rank-1 kernels (all are parity-tested).
-bool use_blocked(int N) {
-  static const int mode = [] {
-    const char* v = std::getenv("RBNS_NEWTON");
-    if (!v || !*v) return 0;
-    return std::strcmp(v, "bgj") == 0 ? 1 : 2;
-  }();
-  return mode == 1 || (mode == 0 && N > 88 && N <= 103);
-}
-
 // tiled Gauss–Jordan kernel (rbns_tgj.cuh): RT = ⌈N/8⌉ row tiles, CT = ⌈(N+1)/8⌉ column tiles, NW warps
 struct TShape {
   int rt, ct, nw;
   NewtonKernel kern;
   size_t base;  // shared memory before the J staging buffer
+  int minb;     // resident CTAs per SM (persistent grid = minb × SMs)
 };
-#define RBNS_TS(R_, C_, W_) {R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>()}
+#define RBNS_TS(R_, C_, W_) \
+  {R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>(), tgj_min_blocks<R_>()}
 const TShape kTShapes[] = {
     RBNS_TS(13, 13, 4),  // 96 < N ≤ 103 (config 2 / 4: N = 100)
+    RBNS_TS(12, 13, 4),  // N = 96
+    RBNS_TS(12, 12, 4),  // 88 < N < 96
+    RBNS_TS(7, 7, 4),    // 48 < N ≤ 55 (config 1: N = 50)
 };
 #undef RBNS_TS
 
@@ -153,7 +92,7 @@ const TShape* tplan(int N) {
 // N > 127: the 2-CTA cluster kernel (rbns_newton_cluster.cuh), 16×(2×16) threads, N ≤ 207
 constexpr int kClusterMaxN = 207;
 
-bool newton_supported(int N) { return plan(N) != nullptr || bplan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
+bool newton_supported(int N) { return plan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
 
 int newton_layout(int N) { return tplan(N) != nullptr ? 1 : 0; }
 
@@ -168,10 +107,6 @@ cudaError_t newton_prepare(int N) {
     e = cudaFuncSetAttribute(t->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(t->kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-  }
-  if (const BShape* b = bplan(N)) {
-    e = cudaFuncSetAttribute(b->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(b->smem));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -195,17 +130,11 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
       cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
       if (e != cudaSuccess) return e;
       const size_t smem = t->base + size_t(p.ldj) * sizeof(double);
-      t->kern<<<std::min(p.n, 2 * p.num_sms), t->nw * 32, smem, st>>>(p);
+      t->kern<<<std::min(p.n, t->minb * p.num_sms), t->nw * 32, smem, st>>>(p);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       *launches = 2;
       return launch_exact(s, p, st);
-    }
-  }
-  if (!p.prefer_rank1 && !p.jl && use_blocked(p.N)) {
-    if (const BShape* b = bplan(p.N)) {
-      b->kern<<<p.n, b->nw * 32, b->smem, st>>>(p);
-      return cudaGetLastError();
     }
   }
   const Shape* s = plan(p.N);
