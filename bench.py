@@ -46,12 +46,19 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (default: the config's)")
-    ap.add_argument("--cpu-sample", type=int, default=65536,
-                    help="μ samples in the cpu_baseline leg (≈10–30 s of host work at cfg 2)")
-    ap.add_argument("--ref-sample", type=int, default=16384,
-                    help="μ samples per step of --impl reference (bounded so the run ends in minutes)")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="μ samples in the cpu_baseline leg (default ≈10–30 s of host work: 65536 at cfg 2, "
+                         "scaled by the per-sample work of other configs)")
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="μ samples per step of --impl reference (default 16384 at cfg 2, scaled likewise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
+
+
+def work_scaled(cfg, at_cfg2: int) -> int:
+    """A CPU sample size with about the host work of ``at_cfg2`` samples of config 2 (per-sample work ∝ Q N³)."""
+    w = cfg.q * cfg.n ** 3 / (7 * 100 ** 3)
+    return int(max(256, min(cfg.batch, at_cfg2 / max(w, 1e-9))))
 
 
 def dist_env():
@@ -210,7 +217,7 @@ def run_reference(args, cfg, world, rank):
     model = synthetic.config_model(cfg)
     batch = args.batch or cfg.batch
     mu = synthetic.config_mu(cfg) if batch <= cfg.batch else synthetic.make_mu(batch, cfg.re_max)
-    sample = min(args.ref_sample, batch)
+    sample = min(args.ref_sample or work_scaled(cfg, 16384), batch)
     S = oracle.symmetrised_operator(model)
     for _ in range(args.warmup):
         oracle.solve_batch(model, mu[:min(64, sample)], tol=cfg.tol, max_iter=cfg.max_iter, S=S)
@@ -290,6 +297,18 @@ def run_ours(args, cfg, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
 
+    # ---- per-sample results do not depend on the batch they are solved in (so an N-GPU μ-sharded run is
+    #      bitwise the 1-GPU run of the same samples): re-solve a 1000-sample subset of this rank's shard
+    #      alone and compare every bit (outside the timed region) ----
+    sub = min(1000, batch)
+    solo = dm.solve(mu[:sub], tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure)
+    ok = bool(torch.equal(solo.u, res.u[:sub]) and torch.equal(solo.iters, res.iters[:sub])
+              and (not pressure or torch.equal(solo.p, res.p[:sub])))
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    if dist is not None:
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    subset_ok = bool(flag.item())
+
     # ---- end-to-end through the C-ABI with host buffers (pinned μ in, results out) ----
     mu_pin = torch.from_numpy(mu_np).pin_memory()
     n, npr = cfg.n, cfg.n_p
@@ -360,8 +379,9 @@ def run_ours(args, cfg, world, rank, local):
                 "roofline": roof, "roofline_e2e": roof_e2e, "newton_update": newton, "gpu_launches": launches, "clocks": clocks.summary(),
                 "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
                            "converged": int((res.status == 0).sum().item()), "batch": batch}}
+        line["bitwise_subset_check"] = subset_ok
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is timed at N = 1 only
-            line["cpu_baseline"] = cpu_baseline(cfg, model, mu_np, min(args.cpu_sample, batch))
+            line["cpu_baseline"] = cpu_baseline(cfg, model, mu_np, min(args.cpu_sample or work_scaled(cfg, 65536), batch))
         print(json.dumps(line), flush=True)
     dm.close()
     if dist is not None:

@@ -153,7 +153,7 @@ namespace {
 // launch helpers
 // -------------------------------------------------------------------------------------------------------
 using ContractKernel = void (*)(const CUtensorMap, const ContractParams);
-constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN, RBNS_SCALE_A_DEFAULT>;
+constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN>;
 
 int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n, const double* u, const double* mu,
                     double* out, int64_t ldo, cudaStream_t st, bool linear_only = false,

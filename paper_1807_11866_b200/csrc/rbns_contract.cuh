@@ -57,9 +57,6 @@ struct ContractParams {
 #ifndef RBNS_WN
 #define RBNS_WN 4
 #endif
-#ifndef RBNS_SCALE_A_DEFAULT
-#define RBNS_SCALE_A_DEFAULT 0
-#endif
 #ifndef RBNS_WM
 #define RBNS_WM 2
 #endif
@@ -74,12 +71,11 @@ __host__ inline size_t contract_smem_bytes(int stages, int ldu, int qb, int ql) 
          size_t(qb + ql) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
 }
 
-// SCALE_A = 0 (default): θ applied once per term to a second accumulator set (168 registers, one CTA per SM).
-// SCALE_A = 1: θ applied to the A fragments, one accumulator set (fewer registers; with MINB = 2 ≤ 112, room
-// for a co-resident Newton-update CTA).  Measured: a contraction/Newton overlap on two streams with that
-// variant ran 273 ms per cfg-2 step against 217 ms sequential (both kernels dilate: the DMMAs and the Newton
-// DFMAs share the FP64 datapath), so the library runs the default variant, one kernel at a time.
-template <int BM, int BN, int WM, int WN, int SCALE_A = 0, int MINB = 1>
+// θ is applied once per term to a second accumulator set (168 registers, one CTA per SM).  Measured and not
+// kept: θ applied to the A fragments (one accumulator set, fewer registers) with a co-resident Newton-update
+// CTA on a second stream ran 273 vs 217 ms per config-2 step (the DMMAs and the Newton FP64 work share the FP64
+// datapath), so the library runs one kernel at a time.
+template <int BM, int BN, int WM, int WN, int MINB = 1>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     contract_kernel(const __grid_constant__ CUtensorMap tmap, const ContractParams p) {
   constexpr int NCW = WM * WN;
@@ -177,53 +173,6 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-    if constexpr (SCALE_A) {
-    // θ applied to the A fragments (one DMUL per fragment): a single accumulator set, fewer registers
-    int q = 0, k0 = 0;
-    double thq[MI];
-#pragma unroll
-    for (int mi = 0; mi < MI; ++mi) thq[mi] = thS[sb0 + mi * 8 + g];
-    for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
-      mbar_wait(&full[stage], phase);
-      const double* st = Sst + size_t(stage) * STAGE;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int kap = 8 * c + 4 * j;
-        if (kap >= 4 * p.nsub) break;
-        if (kap < 4 * p.sub_begin) continue;
-        double af[MI], bf[NI];
-        if (kap < kterms) {
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi) af[mi] = thq[mi] * Us[(sb0 + mi * 8 + g) * p.ldu_s + k0 + t];
-          k0 += 4;
-          if (k0 == p.Ne) {
-            k0 = 0;
-            ++q;
-            if (q < p.Qb) {
-#pragma unroll
-              for (int mi = 0; mi < MI; ++mi) thq[mi] = thS[q * BM + sb0 + mi * 8 + g];
-            }
-          }
-        } else {
-          const int lin = kap - kterms + t;
-#pragma unroll
-          for (int mi = 0; mi < MI; ++mi) af[mi] = lin < p.Ql ? thnuS[lin * BM + sb0 + mi * 8 + g] : 0.0;
-        }
-#pragma unroll
-        for (int ni = 0; ni < NI; ++ni) bf[ni] = st[(j * BN + rb0 + ni * 8 + g) * 4 + t];
-#pragma unroll
-        for (int mi = 0; mi < MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == p.stages) {
-        stage = 0;
-        phase ^= 1u;
-      }
-    }
-    } else {
     double accq[MI][NI][2];
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi)
@@ -284,7 +233,6 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
         stage = 0;
         phase ^= 1u;
       }
-    }
     }
     // epilogue: fragment (sample g, rows 2t..2t+1) -> out[sample][row] as 16-byte stores
 #pragma unroll

@@ -205,6 +205,44 @@ def test_cfg3_slice_oracle_parity(cfg_model, dms):
     print(f"cfg3 slice (1024): max per-sample rel err u {per_sample.max():.2e}, count mismatches {len(mism)}")
 
 
+def test_cfg3_full_batch(cfg_model, dms):
+    """Config 3 at its full size (N = 200, Q = 13, B = 131 072): every sample converges, the solve is bitwise
+    deterministic, the Newton residual at the solution is ≤ 1e-9·‖f(μ)‖ for every sample, and 8 192 samples —
+    the first 4 096 and the last 4 096 of the seeded stream — match the oracle (≤ 1e-10 per sample, identical
+    Newton counts up to knife-edge samples)."""
+    cfg = synthetic.CONFIGS[3]
+    model = cfg_model(3)
+    dm = dms(3, model)
+    mu = synthetic.config_mu(cfg)
+    mud = torch.from_numpy(mu).cuda()
+    a = dm.solve(mud)
+    ua, ita = a.u.clone(), a.iters.clone()
+    b = dm.solve(mud)
+    torch.cuda.synchronize()
+    assert torch.equal(b.u, ua) and torch.equal(b.iters, ita)              # bitwise determinism
+    st = a.status.cpu().numpy()
+    assert np.all(st == 0), np.bincount(st)
+    # residual ≤ 1e-9 ‖f(μ)‖ at every solution (device reduced_operator, chunks of 4096)
+    worst = 0.0
+    for c0 in range(0, len(mu), 4096):
+        R, _ = dm.reduced_operator(mu[c0:c0 + 4096], ua[c0:c0 + 4096])
+        f = oracle.weights(model, mu[c0:c0 + 4096])["load"] @ model.f
+        worst = max(worst, float((np.linalg.norm(R.cpu().numpy(), axis=1) / np.linalg.norm(f, axis=1)).max()))
+    assert worst <= 1e-9, worst
+    idx = np.r_[0:4096, len(mu) - 4096:len(mu)]
+    ur, itr, str_ = threaded_oracle(model, mu[idx], chunk=16)
+    assert np.all(str_ == 0)
+    u = ua.cpu().numpy()[idx]
+    it = ita.cpu().numpy()[idx]
+    per_sample = np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)
+    assert per_sample.max() <= REL, per_sample.max()
+    mism = np.nonzero(it != itr)[0]
+    assert len(mism) <= 16, len(mism)
+    check_counts(model, mu[idx][mism], it[mism], itr[mism])
+    print(f"cfg3 full batch: residual/||f|| max {worst:.2e}; 8192 head+tail samples vs oracle: max rel err "
+          f"{per_sample.max():.2e}, count mismatches {len(mism)}; iteration histogram {np.bincount(ita.cpu().numpy()).tolist()}")
+
+
 @pytest.mark.parametrize("c", [1, 2, 4])
 def test_full_batch_oracle_parity(cfg_model, dms, c):
     """Every sample of configs 1 (16 384), 2 (65 536: the benchmark's workload) and 4 (65 536, with pressure
