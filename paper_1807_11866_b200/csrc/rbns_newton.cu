@@ -3,7 +3,8 @@
 //   tiled Gauss–Jordan (rbns_tgj.cuh)      default where a shape is instantiated (N = 49..55, 89..103)
 //   speculative rank-1 (rbns_newton_spec)   other N ≤ 127, hinted pivot order, misses → exact kernel
 //   exact rank-1 (rbns_newton2.cuh)         full partial-pivot search: every miss of the speculative kernels
-//   2-CTA cluster (rbns_newton_cluster)     127 < N ≤ 207
+//   hybrid tiled Gauss–Jordan (rbns_tgh.cuh) N = 200 (config 3): one CTA per sample, registers + shared memory
+//   2-CTA cluster (rbns_newton_cluster)     other 127 < N ≤ 207, and the exact path of the hybrid kernel
 // RBNS_NEWTON=gjs forces the speculative rank-1 kernels, RBNS_NEWTON=gj2 the exact one (parity-tested).
 #include "rbns_launch.h"
 #include <algorithm>
@@ -15,6 +16,7 @@
 #include "rbns_newton_spec.cuh"
 #include "rbns_newton_cluster.cuh"
 #include "rbns_tgj.cuh"
+#include "rbns_tgh.cuh"
 
 namespace rbns {
 
@@ -87,6 +89,29 @@ const TShape* tplan(int N) {
     if (s.rt == rt && s.ct == ct) return &s;
   return nullptr;
 }
+
+// hybrid tiled kernel (rbns_tgh.cuh): N = 8·RT exactly, 12 warps, one CTA per SM
+struct HShape {
+  int rt, nw;
+  NewtonKernel kern;
+  size_t smem;
+};
+const HShape kHShapes[] = {
+    {25, 12, newton_tgh_kernel<25, 12>, tgh_smem_bytes<25, 12>()},  // N = 200 (config 3)
+    {7, 3, newton_tgh_kernel<7, 3>, tgh_smem_bytes<7, 3>()},        // N = 56, RBNS_NEWTON=tgh only (tests)
+    {13, 6, newton_tgh_kernel<13, 6>, tgh_smem_bytes<13, 6>()},     // N = 104, RBNS_NEWTON=tgh only (tests)
+};
+const HShape* hplan(int N) {
+  static const int mode = [] {  // 0: default (config-3 shape), 1: off, 2: every instantiated shape (tests)
+    const char* v = std::getenv("RBNS_NEWTON");
+    if (!v || !*v || std::strcmp(v, "tgj") == 0) return 0;
+    return std::strcmp(v, "tgh") == 0 ? 2 : 1;
+  }();
+  if (mode == 1) return nullptr;
+  for (const HShape& s : kHShapes)
+    if (N == 8 * s.rt && (mode == 2 || &s == &kHShapes[0])) return &s;
+  return nullptr;
+}
 }  // namespace
 
 // N > 127: the 2-CTA cluster kernel (rbns_newton_cluster.cuh), 16×(2×16) threads, N ≤ 207
@@ -94,7 +119,7 @@ constexpr int kClusterMaxN = 207;
 
 bool newton_supported(int N) { return plan(N) != nullptr || (N >= 1 && N <= kClusterMaxN); }
 
-int newton_layout(int N) { return tplan(N) != nullptr ? 1 : 0; }
+int newton_layout(int N) { return tplan(N) != nullptr || hplan(N) != nullptr ? 1 : 0; }
 
 cudaError_t newton_prepare(int N) {
   int dev = 0, max_smem = 0;
@@ -107,6 +132,13 @@ cudaError_t newton_prepare(int N) {
     e = cudaFuncSetAttribute(t->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(t->kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+  }
+  if (const HShape* h = hplan(N)) {
+    if (h->smem > size_t(max_smem)) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(h->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(h->smem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(h->kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -137,6 +169,22 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
       return launch_exact(s, p, st);
     }
   }
+  if (!p.prefer_rank1 && p.jl) {
+    if (const HShape* h = hplan(p.N)) {
+      cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
+      if (e != cudaSuccess) return e;
+      h->kern<<<std::min(p.n, p.num_sms), h->nw * 32, h->smem, st>>>(p);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      // the samples it handed back: the exact cluster kernel over the device-side list
+      NewtonParams q = p;
+      q.sub = p.miss_list;
+      q.n_sub = p.miss_count;
+      newton_gjc_kernel<16, 16, 13, 7><<<2 * std::min(p.n, std::max(1, p.num_sms / 2)), 256, 0, st>>>(q);
+      *launches = 2;
+      return cudaGetLastError();
+    }
+  }
   const Shape* s = plan(p.N);
   if (!s && p.N <= kClusterMaxN) {
     newton_gjc_kernel<16, 16, 13, 7><<<2 * p.n, 256, 0, st>>>(p);
@@ -159,6 +207,11 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
 
 }  // namespace rbns
 
+#ifdef RBNS_TGH_DUMP
+extern "C" int rbns_debug_tgh(double* out) {
+  return cudaMemcpyFromSymbol(out, rbns::g_tgh_dump, sizeof(double) * 4 * 256) == cudaSuccess ? 0 : 2;
+}
+#endif
 #ifdef RBNS_TRACE
 extern "C" int rbns_debug_trace(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, rbns::g_trace, sizeof(unsigned long long) * (n < 256 ? n : 256)) == cudaSuccess ? 0 : 2;

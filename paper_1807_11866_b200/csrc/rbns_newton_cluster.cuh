@@ -230,31 +230,22 @@ __device__ __forceinline__ void gjcs_block(double (&a)[RS][CS], unsigned& pmask,
   }
 }
 
+// One sample (chunk position i_s) on this cluster; the caller's loop keeps both CTAs on the same positions.
 template <int TGR, int TGC, int RS, int CS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
-    newton_gjc_kernel(const NewtonParams p) {
+__device__ __forceinline__ void gjc_sample(const NewtonParams& p, const int i_s, GJCShared<TGR, TGC, RS, CS>& sh,
+                                           GJCShared<TGR, TGC, RS, CS>* peer, const int rank) {
   namespace cg = cooperative_groups;
   constexpr int NT = TGR * TGC;
   constexpr int NW = NT / 32;
-  static_assert(TGR == 16 && NT % 32 == 0, "owner half-warp layout needs TGR = 16");
-  __shared__ GJCShared<TGR, TGC, RS, CS> sh;
   cg::cluster_group cluster = cg::this_cluster();
-  const int rank = int(cluster.block_rank());
-  GJCShared<TGR, TGC, RS, CS>* peer = cluster.map_shared_rank(&sh, rank ^ 1);
-  const int i_s = blockIdx.x / 2;
-  const bool live = i_s < p.n;  // both CTAs of a cluster agree
-  const int b = live ? p.act[i_s] : 0;
+  const int b = p.act[i_s];
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
   const int rhs_rank = (N % (2 * TGC)) / TGC, rhs_tc = N % TGC, rhs_slot = N / (2 * TGC);
   auto gcol = [&](int s) { return s * 2 * TGC + rank * TGC + tc; };
 
-  if (live) newton_weights(p, b, sh.w);
+  newton_weights(p, b, sh.w);
   __syncthreads();
-  if (!live) {
-    cluster.sync();
-    return;
-  }
   double a[RS][CS];
   const double* Jb = p.J + int64_t(i_s) * p.ldj;
   // J into registers and the right-hand side as column N (rank rhs_rank); called again by the exact path
@@ -415,6 +406,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
     for (int i = tid; i < N; i += NT) p.hint_out[int64_t(b) * N + i] = int16_t(sh.perm[i]);
   }
   cluster.sync();  // the peer may still read this CTA's shared memory
+}
+
+// Grid: two CTAs per position.  p.sub == NULL: positions 0 .. n-1, one per cluster (grid 2n).  p.sub != NULL:
+// the listed positions sub[0 .. *n_sub) (the samples a tiled kernel handed back), strided over the grid's
+// clusters, so the grid need not know the device-side count.
+template <int TGR, int TGC, int RS, int CS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TGR * TGC, 1)
+    newton_gjc_kernel(const NewtonParams p) {
+  namespace cg = cooperative_groups;
+  static_assert(TGR == 16 && (TGR * TGC) % 32 == 0, "owner half-warp layout needs TGR = 16");
+  __shared__ GJCShared<TGR, TGC, RS, CS> sh;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = int(cluster.block_rank());
+  GJCShared<TGR, TGC, RS, CS>* peer = cluster.map_shared_rank(&sh, rank ^ 1);
+  const int cnt = p.sub ? *p.n_sub : p.n;
+#pragma unroll 1
+  for (int k = int(blockIdx.x / 2); k < cnt; k += int(gridDim.x / 2))
+    gjc_sample<TGR, TGC, RS, CS>(p, p.sub ? p.sub[k] : k, sh, peer, rank);
 }
 
 }  // namespace rbns

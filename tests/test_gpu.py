@@ -191,7 +191,8 @@ def threaded_oracle(model, mu, chunk=64):
 
 
 def test_cfg3_slice_oracle_parity(cfg_model, dms):
-    """Config 3 (N = 200, Q = 13: the 2-CTA cluster Newton kernel, S streamed from HBM) on a 1024-sample slice."""
+    """Config 3 (N = 200, Q = 13: the hybrid register/shared-memory tiled Newton kernel, S streamed from HBM) on a
+    1024-sample slice."""
     cfg = synthetic.CONFIGS[3]
     model = cfg_model(3)
     mu = synthetic.config_mu(cfg, 1024)
@@ -520,7 +521,7 @@ def test_concurrent_streams(cfg_model, dms):
     assert a.stats["sample_iterations"] == int(a.iters.sum()) and b.stats["sample_iterations"] == int(b.iters.sum())
 
 
-@pytest.mark.parametrize("n", [40, 100, 150])
+@pytest.mark.parametrize("n", [40, 100, 150, 200])
 def test_pivot_hint_misses_take_the_exact_path(n):
     """Rows of A₀ permuted: partial pivoting picks a non-identity order, so the speculative kernel's identity hint
     fails at the first Newton iteration and every sample is re-run by the exact full-search kernel; from the
@@ -557,7 +558,7 @@ def test_alternate_newton_kernels(variant):
         "import numpy as np, torch\n"
         "from oracle import rbns_oracle as o\n"
         "from paper_1807_11866_b200 import online, synthetic\n"
-        "for c, nb in ((1, 256), (2, 96)):\n"
+        "for c, nb in ((1, 256), (2, 96), (3, 24)):\n"
         "    cfg = synthetic.CONFIGS[c]; m = synthetic.config_model(cfg); mu = synthetic.config_mu(cfg, nb)\n"
         "    with online.DeviceModel(m, 0) as dm:\n"
         "        r = dm.solve(torch.from_numpy(mu).cuda()); torch.cuda.synchronize()\n"
@@ -572,6 +573,32 @@ def test_alternate_newton_kernels(variant):
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 
+
+def test_hybrid_kernel_test_shapes():
+    """The hybrid register/shared-memory tiled kernel (rbns_tgh.cuh, config 3's N = 200) at its two small test
+    shapes (N = 56: 3 warps, N = 104: 6 warps; RBNS_NEWTON=tgh) against the oracle, batch over several CTA waves."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import rbns_oracle as o\n"
+        "from paper_1807_11866_b200 import online, synthetic\n"
+        "for n in (56, 104):\n"
+        "    m = synthetic.make_model(n, 3, 'trig3', seed=n); mu = synthetic.make_mu(400, 50.0, seed=n)\n"
+        "    with online.DeviceModel(m, 0) as dm:\n"
+        "        r = dm.solve(torch.from_numpy(mu).cuda()); torch.cuda.synchronize()\n"
+        "    ur, itr, st, _ = o.solve_batch(m, mu)\n"
+        "    u = r.u.cpu().numpy(); it = r.iters.cpu().numpy()\n"
+        "    assert np.all(st == 0) and np.all(r.status.cpu().numpy() == 0), n\n"
+        "    assert (np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)).max() <= 1e-10, n\n"
+        "    assert (it != itr).sum() <= 1, n\n"
+        "print('ok')\n")
+    env = dict(os.environ, RBNS_NEWTON="tgh")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
 def test_unsupported_size_fails_loudly():
     """N beyond the register/cluster Newton kernels (207) is rejected at model creation, not computed wrong."""

@@ -1,6 +1,7 @@
 #!/bin/bash
 # One GPU session: bench line (+ reference arm), plain run + ncu launch list of one bench step, full ncu capture
-# of the two hot kernels (contraction + Newton update) on a fixed cfg-2 workload.
+# of the two hot kernels (contraction + tiled Newton update) on a fixed cfg-2 workload, and of the cfg-3 Newton
+# kernel on a 4096-sample cfg-3 workload.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt
@@ -12,5 +13,8 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 P="python tools/profile_case.py 2 65536"
 $P > gpurun_out/plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"contract_kernel" -s 2 -c 1 -o gpurun_out/full $P > gpurun_out/ncu_full.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"newton_bgj" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+  ncu --set full --clock-control none --import-source on -k regex:"newton_tgj" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
+P3="python tools/profile_case.py 3 4096"
+$P3 > gpurun_out/plain3.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"newton_" -s 2 -c 1 -o gpurun_out/full_lu3 $P3 > gpurun_out/ncu_full_lu3.log 2>&1
+tail -2 gpurun_out/ncu_full.log gpurun_out/ncu_full_lu.log gpurun_out/ncu_full_lu3.log
