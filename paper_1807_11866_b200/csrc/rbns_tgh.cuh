@@ -90,6 +90,54 @@ __device__ __forceinline__ bool tgh_verify(int P, const double2 wv, const double
   return __any_sync(0xffffffffu, bad) != 0;
 }
 
+// Panel P (W_P = Ws, pivot column M) into this warp's selected tiles: shared tile T0 (A0), the register tile
+// (A1), shared tile T2 (A2).  X_k = W_P J_Pk per tile, then one load of M_i per row tile for all of them.
+template <int RT, int A0, int A1, int A2>
+__device__ __forceinline__ void tgh_apply(double (&acc)[RT][2], double* T0, double* T2, const double* Ws,
+                                          const double (*M)[64], int P) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const double2 wv = *reinterpret_cast<const double2*>(&Ws[tgj_slot(g, 2 * t)]);
+  double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0, x20 = 0.0, x21 = 0.0;
+  if constexpr (A0 != 0) {
+    const double2 pv = *reinterpret_cast<const double2*>(T0 + 64 * P + 2 * lane);
+    dmma_8x8x4(x00, x01, pv.x, wv.x);
+    dmma_8x8x4(x00, x01, pv.y, wv.y);
+  }
+  if constexpr (A1 != 0) {
+    double q0, q1;
+    tgh_pick<RT>(acc, P, q0, q1);
+    dmma_8x8x4(x10, x11, q0, wv.x);
+    dmma_8x8x4(x10, x11, q1, wv.y);
+  }
+  if constexpr (A2 != 0) {
+    const double2 pv = *reinterpret_cast<const double2*>(T2 + 64 * P + 2 * lane);
+    dmma_8x8x4(x20, x21, pv.x, wv.x);
+    dmma_8x8x4(x20, x21, pv.y, wv.y);
+  }
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const double2 m = *reinterpret_cast<const double2*>(&M[i][tgj_slot(g, 2 * t)]);
+    if constexpr (A1 != 0) {
+      dmma_8x8x4(acc[i][0], acc[i][1], x10, m.x);
+      dmma_8x8x4(acc[i][0], acc[i][1], x11, m.y);
+    }
+    if constexpr (A0 != 0) {
+      double2* c = reinterpret_cast<double2*>(T0 + 64 * i + 2 * lane);
+      double2 v = *c;
+      dmma_8x8x4(v.x, v.y, x00, m.x);
+      dmma_8x8x4(v.x, v.y, x01, m.y);
+      *c = v;
+    }
+    if constexpr (A2 != 0) {
+      double2* c = reinterpret_cast<double2*>(T2 + 64 * i + 2 * lane);
+      double2 v = *c;
+      dmma_8x8x4(v.x, v.y, x20, m.x);
+      dmma_8x8x4(v.x, v.y, x21, m.y);
+      *c = v;
+    }
+  }
+}
+
 #ifdef RBNS_TGH_DUMP  // development: sample position 0's right-hand side, final y column and δ
 __device__ double g_tgh_dump[4][256];
 #endif
@@ -247,45 +295,17 @@ __global__ void __launch_bounds__(NW * 32, 1) newton_tgh_kernel(const NewtonPara
     // of M_i for all of them.  The pivot row tile (M_P = 0) is left as it is.
     auto apply = [&](int P, bool a0, bool a1, bool a2) {
       const int s = (pc0 + P) % NB;
-      const double2 wv = *reinterpret_cast<const double2*>(&sh.W[s][tgj_slot(g, 2 * t)]);
-      double x00 = 0.0, x01 = 0.0, x10 = 0.0, x11 = 0.0, x20 = 0.0, x21 = 0.0;
-      if (a0) {
-        const double2 pv = *reinterpret_cast<const double2*>(T0 + 64 * P + 2 * lane);
-        dmma_8x8x4(x00, x01, pv.x, wv.x);
-        dmma_8x8x4(x00, x01, pv.y, wv.y);
-      }
-      if (a1) {
-        double q0, q1;
-        tgh_pick<RT>(acc, P, q0, q1);
-        dmma_8x8x4(x10, x11, q0, wv.x);
-        dmma_8x8x4(x10, x11, q1, wv.y);
-      }
-      if (a2) {
-        const double2 pv = *reinterpret_cast<const double2*>(T2 + 64 * P + 2 * lane);
-        dmma_8x8x4(x20, x21, pv.x, wv.x);
-        dmma_8x8x4(x20, x21, pv.y, wv.y);
-      }
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const double2 m = *reinterpret_cast<const double2*>(&sh.M[s][i][tgj_slot(g, 2 * t)]);
-        if (a1) {
-          dmma_8x8x4(acc[i][0], acc[i][1], x10, m.x);
-          dmma_8x8x4(acc[i][0], acc[i][1], x11, m.y);
-        }
-        if (a0) {
-          double2* c = reinterpret_cast<double2*>(T0 + 64 * i + 2 * lane);
-          double2 v = *c;
-          dmma_8x8x4(v.x, v.y, x00, m.x);
-          dmma_8x8x4(v.x, v.y, x01, m.y);
-          *c = v;
-        }
-        if (a2) {
-          double2* c = reinterpret_cast<double2*>(T2 + 64 * i + 2 * lane);
-          double2 v = *c;
-          dmma_8x8x4(v.x, v.y, x20, m.x);
-          dmma_8x8x4(v.x, v.y, x21, m.y);
-          *c = v;
-        }
+      // compile-time tile selection: a runtime flag would be if-converted and the DMMAs of dead tiles issued
+      const int sel = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0);
+      switch (sel) {
+        case 1: tgh_apply<RT, 1, 0, 0>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 2: tgh_apply<RT, 0, 1, 0>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 3: tgh_apply<RT, 1, 1, 0>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 4: tgh_apply<RT, 0, 0, 1>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 5: tgh_apply<RT, 1, 0, 1>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 6: tgh_apply<RT, 0, 1, 1>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        case 7: tgh_apply<RT, 1, 1, 1>(acc, T0, T2, sh.W[s], sh.M[s], P); break;
+        default: break;
       }
     };
     // panel P into the live tiles other than slot `skip`, verification, release of the slot
