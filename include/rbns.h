@@ -18,6 +18,8 @@
  *   rbns_recover_pressure    <- solve_block step 2, B_sp p = f_s - A_sv u
  *   rbns_reconstruct_pressure<- online.reconstruct_pressure, combined scheme: p = P_att u with the model's
  *                               attached pressure modes
+ *   rbns_project_convection  <- build_reduced_model's c-term contraction C_jkl = c(ψ_j, ψ_k, ψ_l) (offline,
+ *                               SPEC.md:449-457; reference assemble.py:86-101 convection_matrices)
  *   rbns_error_string        <- errors.RbflowError messages (reference errors.py:4-21)
  *
  * All arrays are IEEE fp64 (or the stated integer type), row-major, C-contiguous.  "dev" pointers are CUDA
@@ -210,6 +212,15 @@ int rbns_reconstruct_pressure(rbns_model* model, const double* u, int64_t batch,
 int rbns_model_attached(const rbns_model* model, int32_t* n_att);
 
 int rbns_get_stats(const rbns_model* model, rbns_stats* out);
+
+/* Offline projection of one convective term onto a reduced basis tabulated at P quadrature points (device
+ * buffers on the current device, stream-ordered; no model handle):
+ *   C[j][k][l] = sum_p w[p] sum_{c,d} val_u[p][d][j] * grad[p][c][d][k] * val_w[p][c][l]
+ *   val_u dev P x 2 x N (advecting functions), grad dev P x 2 x 2 x N (grad[p][c][d][k] = d_d psi_{k,c}),
+ *   val_w dev P x 2 x N (test functions), w dev P (quadrature weight x |det|), C dev N x N x N.
+ * splits: split-K slices over the points (0: automatic); the slices are summed in a fixed order (deterministic). */
+int rbns_project_convection(const double* val_u, const double* grad, const double* val_w, const double* w,
+                            int64_t points, int32_t n, double* C, int32_t splits, void* stream);
 
 const char* rbns_error_string(int code);
 const char* rbns_last_error_message(void);

@@ -25,7 +25,8 @@ EXPORTED_SYMBOLS = (
     "rbns_model_create", "rbns_model_create2", "rbns_model_terms", "rbns_model_destroy", "rbns_model_info",
     "rbns_model_device_bytes", "rbns_model_attached", "rbns_solve", "rbns_solve_ex", "rbns_solve_host",
     "rbns_solve_host_ex", "rbns_reduced_operator", "rbns_recover_pressure", "rbns_reconstruct_pressure",
-    "rbns_get_stats", "rbns_error_string", "rbns_last_error_message", "rbns_abi_version",
+    "rbns_get_stats", "rbns_project_convection", "rbns_error_string", "rbns_last_error_message",
+    "rbns_abi_version",
 )
 ABI_VERSION = 3
 ERR_NO_ATTACHED = 6
@@ -102,6 +103,7 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.rbns_reduced_operator.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     lib.rbns_recover_pressure.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     lib.rbns_get_stats.argtypes = [vp, ctypes.POINTER(StatsC)]
+    lib.rbns_project_convection.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp]
     lib.rbns_error_string.argtypes = [ctypes.c_int]
     lib.rbns_error_string.restype = ctypes.c_char_p
     lib.rbns_last_error_message.argtypes = []

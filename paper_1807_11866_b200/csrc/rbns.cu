@@ -34,6 +34,11 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace
+
+int rbns::set_last_error(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
 
 #define RBNS_CUDA(call)                                                                                  \
   do {                                                                                                   \

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "rbns_common.cuh"
 
 namespace rbns {
@@ -16,5 +18,8 @@ int newton_layout(int N);
 cudaError_t newton_prepare(int N);
 // launches the Newton-update kernel(s) for p on st; *launches receives the number of kernels launched
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches);
+
+// records msg as the calling thread's rbns_last_error_message() and returns code (entry points outside rbns.cu)
+int set_last_error(int code, const std::string& msg);
 
 }  // namespace rbns

@@ -16,5 +16,8 @@ $P > gpurun_out/plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"newton_tgj" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
 P3="python tools/profile_case.py 3 4096"
 $P3 > gpurun_out/plain3.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"newton_" -s 2 -c 1 -o gpurun_out/full_lu3 $P3 > gpurun_out/ncu_full_lu3.log 2>&1
-tail -2 gpurun_out/ncu_full.log gpurun_out/ncu_full_lu.log gpurun_out/ncu_full_lu3.log
+  ncu --set full --clock-control none --import-source on -k regex:"newton_tgh" -s 2 -c 1 -o gpurun_out/full_lu3 $P3 > gpurun_out/ncu_full_lu3.log 2>&1
+for f in gpurun_out/ncu_full.log gpurun_out/ncu_full_lu.log gpurun_out/ncu_full_lu3.log; do tail -n 2 $f; done
+# offline projection kernel: throughput line + one full capture
+python tools/projection_perf.py 100 262144 > gpurun_out/projection_perf.txt 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"project_convection" -s 3 -c 1 -o gpurun_out/full_proj python tools/projection_perf.py 100 65536 > gpurun_out/ncu_proj.log 2>&1
