@@ -90,26 +90,34 @@ const TShape* tplan(int N) {
   return nullptr;
 }
 
-// hybrid tiled kernel (rbns_tgh.cuh): N = 8·RT exactly, 12 warps, one CTA per SM
+// hybrid register/shared-memory tiled kernel (rbns_tgh.cuh): RT row tiles, CT column tiles, NW warps, REG =
+// register slots; persistent grid of minb CTAs per SM
 struct HShape {
-  int rt, nw;
+  int rt, ct, nw;
   NewtonKernel kern;
   size_t smem;
+  int minb;
+  bool test_only;  // instantiated for the tests (RBNS_NEWTON=tgh), not the default for its N
 };
+#define RBNS_HS(R_, C_, W_, G_, T_) \
+  {R_, C_, W_, newton_tgh_kernel<R_, C_, W_, G_>, tgh_smem_bytes<R_, C_, W_, G_>(), tgh_min_blocks<W_, G_>(), T_}
 const HShape kHShapes[] = {
-    {25, 12, newton_tgh_kernel<25, 12>, tgh_smem_bytes<25, 12>()},  // N = 200 (config 3)
-    {7, 3, newton_tgh_kernel<7, 3>, tgh_smem_bytes<7, 3>()},        // N = 56, RBNS_NEWTON=tgh only (tests)
-    {13, 6, newton_tgh_kernel<13, 6>, tgh_smem_bytes<13, 6>()},     // N = 104, RBNS_NEWTON=tgh only (tests)
+    RBNS_HS(25, 26, 12, 2, false),  // N = 200 (config 3): 12 register + 13 shared column tiles, 1 CTA/SM
+    RBNS_HS(13, 13, 4, 6, true),    // 96 < N ≤ 103: 2 register + 1 shared tile per warp, 3 CTAs/SM
+    RBNS_HS(7, 8, 3, 2, true),      // N = 56  (tests)
+    RBNS_HS(13, 14, 6, 2, true),    // N = 104 (tests)
 };
+#undef RBNS_HS
 const HShape* hplan(int N) {
-  static const int mode = [] {  // 0: default (config-3 shape), 1: off, 2: every instantiated shape (tests)
+  static const int mode = [] {  // 0: default (config-3 shape), 1: off, 2: every instantiated shape
     const char* v = std::getenv("RBNS_NEWTON");
     if (!v || !*v || std::strcmp(v, "tgj") == 0) return 0;
     return std::strcmp(v, "tgh") == 0 ? 2 : 1;
   }();
-  if (mode == 1) return nullptr;
+  if (mode == 1 || N <= 8) return nullptr;
+  const int rt = (N + 7) / 8, ct = (N + 8) / 8;
   for (const HShape& s : kHShapes)
-    if (N == 8 * s.rt && (mode == 2 || &s == &kHShapes[0])) return &s;
+    if (s.rt == rt && s.ct == ct && (mode == 2 || !s.test_only)) return &s;
   return nullptr;
 }
 }  // namespace
@@ -155,7 +163,7 @@ static cudaError_t launch_exact(const Shape* s, const NewtonParams& p, cudaStrea
 
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches) {
   *launches = 1;
-  if (!p.prefer_rank1 && p.jl) {
+  if (!p.prefer_rank1 && p.jl && !hplan(p.N)) {
     const TShape* t = tplan(p.N);
     const Shape* s = plan(p.N);
     if (t && s && s->exact) {
@@ -173,15 +181,16 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
     if (const HShape* h = hplan(p.N)) {
       cudaError_t e = cudaMemsetAsync(p.miss_count, 0, sizeof(int32_t), st);
       if (e != cudaSuccess) return e;
-      h->kern<<<std::min(p.n, p.num_sms), h->nw * 32, h->smem, st>>>(p);
+      h->kern<<<std::min(p.n, h->minb * p.num_sms), h->nw * 32, h->smem, st>>>(p);
       e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      // the samples it handed back: the exact cluster kernel over the device-side list
+      *launches = 2;
+      // the samples it handed back: the exact kernel over the device-side list
+      if (const Shape* s = plan(p.N); s && s->exact) return launch_exact(s, p, st);
       NewtonParams q = p;
       q.sub = p.miss_list;
       q.n_sub = p.miss_count;
       newton_gjc_kernel<16, 16, 13, 7><<<2 * std::min(p.n, std::max(1, p.num_sms / 2)), 256, 0, st>>>(q);
-      *launches = 2;
       return cudaGetLastError();
     }
   }

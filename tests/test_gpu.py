@@ -585,7 +585,7 @@ def test_hybrid_kernel_test_shapes():
         "import numpy as np, torch\n"
         "from oracle import rbns_oracle as o\n"
         "from paper_1807_11866_b200 import online, synthetic\n"
-        "for n in (56, 104):\n"
+        "for n in (56, 97, 100, 103, 104):\n"
         "    m = synthetic.make_model(n, 3, 'trig3', seed=n); mu = synthetic.make_mu(400, 50.0, seed=n)\n"
         "    with online.DeviceModel(m, 0) as dm:\n"
         "        r = dm.solve(torch.from_numpy(mu).cuda()); torch.cuda.synchronize()\n"

@@ -7,7 +7,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np, torch
 from oracle import rbns_oracle as oracle
 from paper_1807_11866_b200 import online, synthetic
-for n in (56, 104, 200):
+for n in (56, 97, 100, 103, 104, 200):
     m = synthetic.make_model(n, 3, "trig3", seed=n)
     mu = synthetic.make_mu(4, 50.0, seed=n)
     with online.DeviceModel(m, 0) as dm:
