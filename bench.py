@@ -362,13 +362,22 @@ def run_ours(args, cfg, world, rank, local):
         gj_flops = sample_its * 2.0 * n3
         lu_flops = sample_its * ((2.0 / 3.0) * n3 + 2.0 * n2)
         lu_s = float(np.mean(lu_ms)) * 1e-3
-        newton = {"kernel": "newton_tgj_kernel (tiled Gauss-Jordan, 8x8 block pivots, DMMA, TMA-staged J)"
-                  if 96 < cfg.n <= 103 else "Newton update kernels", "ms_per_step": lu_s * 1e3,
+        if cfg.n == 200:
+            nk = ("newton_tgh_kernel (hybrid tiled Gauss-Jordan: 12 register + 13 TMA-fed shared-memory column "
+                  "tiles, 8x8 block pivots, DMMA)")
+            nb = ("DMMA pipe (~70% active, ncu) behind the per-panel chain; one sample per SM (the 322 KB system "
+                  "fills registers + shared memory)")
+        elif 48 < cfg.n <= 55 or 88 < cfg.n <= 103:
+            nk = "newton_tgj_kernel (tiled Gauss-Jordan, 8x8 block pivots, DMMA, TMA-staged J)"
+            nb = ("latency: the per-panel chain (8x8 pivot-tile inversion on one warp, ~13 panels per sample), two "
+                  "samples per SM (register file)")
+        else:
+            nk, nb = "rank-1 Newton kernels (rbns_newton_spec / rbns_newton2)", "latency: the per-column chain"
+        newton = {"kernel": nk, "ms_per_step": lu_s * 1e3,
                   "share_of_step": float(np.sum(lu_ms) / np.sum(step_ms)),
                   "achieved_gj": gj_flops / lu_s / 1e12, "achieved_lu_equivalent": lu_flops / lu_s / 1e12,
                   "peak": peak["tflops"], "unit": "TFLOP/s", "frac_gj": gj_flops / lu_s / 1e12 / peak["tflops"],
-                  "bound": "latency: the per-panel chain (8x8 pivot-tile inversion on one warp, ~13 panels per "
-                           "sample), two samples per SM (register file)"}
+                  "bound": nb}
         line = {"metric": METRIC, "value": batch * world / (max_ms * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -35,6 +35,14 @@ def launch_summary(path):
     for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"{k[:60]:60s} {n:8d} {ms:10.3f} {ms / tot:6.1%}")
     lines.append(f"{'total':60s} {sum(v[0] for v in agg.values()):8d} {tot:10.3f}")
+    # the solver's own kernels only (the step): the cutlass DGEMMs are bench.py's in-run FP64 peak measurement,
+    # the at:: kernels its input generation and L2 flush
+    own = {k: v for k, v in agg.items() if k.startswith("rbns::")}
+    tot_own = sum(v[1] for v in own.values())
+    lines += ["", "solver kernels only (shares of the solve; bench.py's cutlass DGEMMs measure the FP64 peak):",
+              f"{'kernel':60s} {'launches':>8s} {'ms':>10s} {'share':>6s}"]
+    for k, (n, ms) in sorted(own.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"{k[:60]:60s} {n:8d} {ms:10.3f} {ms / tot_own:6.1%}")
     return "\n".join(lines) + "\n"
 
 
