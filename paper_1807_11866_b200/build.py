@@ -34,7 +34,7 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=())
     (e.g. -DRBNS_TRACE for the instrumented development build)."""
     OUT_ = Path(out)
     srcs = sorted(CSRC.glob("*.cu"))
-    deps = srcs + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "rbns.h"]
+    deps = srcs + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "rbns.h"]
     if OUT_.exists() and not force and all(OUT_.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return OUT_
     obj_dir = OBJ if not extra else OBJ.parent / ("obj_" + "_".join(x.strip("-D").lower() for x in extra))
@@ -62,6 +62,15 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=())
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, OUT_)
     return OUT_
+
+
+CHECKED = ROOT / "build" / "librbns_checked.so"
+
+
+def build_checked(force: bool = False) -> Path:
+    """The checked development build (-DRBNS_CHECKED: device-side bounds / protocol checks, readout through
+    rbns_debug_checks) used by tests/test_checked.py in place of compute-sanitizer."""
+    return build(force=force, out=CHECKED, extra=("-DRBNS_CHECKED",))
 
 
 if __name__ == "__main__":

@@ -162,7 +162,7 @@ constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN>;
 
 int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n, const double* u, const double* mu,
                     double* out, int64_t ldo, cudaStream_t st, bool linear_only = false,
-                    const double* wts = nullptr) {
+                    const double* wts = nullptr, int64_t B = 0) {
   if (n <= 0) return RBNS_OK;
   ContractParams p{};
   p.act = act;
@@ -185,6 +185,7 @@ int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n,
   p.out = out;
   p.ldo = ldo;
   p.wts = wts;
+  p.B = B;
   const int sample_tiles = (n + kBM - 1) / kBM;
   // target CTAs per SM over the launch (16 measured best at configs 1 and 2: 4, 8, 12, 16, 24, 32, 64 tried)
   static const int64_t waves = env_int64("RBNS_CONTRACT_WAVES", 16);
@@ -218,7 +219,7 @@ NewtonParams newton_params(const rbns_model* m) {
 int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int64_t ldj, double* u,
                   const double* mu, int iter, int max_iter, double tol, int32_t* iters, int8_t* status, double* last,
                   int16_t* hints, int32_t* spec_miss, int32_t* miss_list, int32_t* miss_count, int* launches,
-                  bool prefer_rank1, cudaStream_t st, const double* wf = nullptr) {
+                  bool prefer_rank1, cudaStream_t st, const double* wf = nullptr, int64_t B = 0) {
   if (n <= 0) return RBNS_OK;
   NewtonParams p = newton_params(m);
   p.act = act;
@@ -240,6 +241,7 @@ int launch_newton(rbns_model* m, const int32_t* act, int n, const double* J, int
   p.miss_count = miss_count;
   p.prefer_rank1 = prefer_rank1 ? 1 : 0;
   p.wf = wf;
+  p.B = B;
   RBNS_CUDA(launch_newton_update(p, st, launches));
   return RBNS_OK;
 }
@@ -436,7 +438,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
         // u = 0 at the first step: the convective part vanishes, only the affine block of the GEMM runs
         // (J = L(μ), h = 0); later steps run the full contraction
         const int e = timer.begin(first ? 3 : 0);
-        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first, wts);
+        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first, wts, B);
         timer.end(e);
         if (rc) break;
         stats.gemm_launches += 1;
@@ -445,7 +447,7 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
       const int e = timer.begin(1);
       int nl = 0;
       rc = launch_newton(m, act0 + c0, nc, jbuf, ldj, u, mu, it, max_iter, tol, iters, status, last, hints,
-                         dcount + 1, miss_list, dcount + 2, &nl, prefer_rank1, st, wf);
+                         dcount + 1, miss_list, dcount + 2, &nl, prefer_rank1, st, wf, B);
       timer.end(e);
       if (rc) break;
       stats.lu_launches += nl;
@@ -974,3 +976,25 @@ int rbns_recover_pressure(rbns_model* m, const double* mu, const double* u, int6
 }
 
 }  // extern "C"
+
+// Checked builds: failed device-side checks of every translation unit (line of the first failure, total count);
+// 0 / 0 in the product build, where the checks compile away.  Not part of the public ABI (include/rbns.h).
+extern "C" int rbns_debug_checks(int* line_main, int* line_newton, unsigned long long* count) {
+  int ln = 0;
+  unsigned long long cn = 0;
+  if (rbns::newton_debug_checks(&ln, &cn)) return 2;
+#ifdef RBNS_CHECKED
+  int lm = 0;
+  unsigned long long cm = 0;
+  if (cudaMemcpyFromSymbol(&lm, rbns::g_chk_line, sizeof(int)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(&cm, rbns::g_chk_count, sizeof(unsigned long long)) != cudaSuccess)
+    return 2;
+  *line_main = lm;
+  *count = cm + cn;
+#else
+  *line_main = 0;
+  *count = cn;
+#endif
+  *line_newton = ln;
+  return 0;
+}

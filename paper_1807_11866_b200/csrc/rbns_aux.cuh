@@ -164,7 +164,10 @@ __global__ void __launch_bounds__(kCompactThreads) compact_active(const int32_t*
     running += __shfl_sync(0xffffffffu, v, 31);
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-      if ((m[j] >> lane) & 1u) act_out[pos + __popc(m[j] & lt)] = id[j];
+      if ((m[j] >> lane) & 1u) {
+        RBNS_CHECK(pos + __popc(m[j] & lt) < n_in);
+        act_out[pos + __popc(m[j] & lt)] = id[j];
+      }
       pos += __popc(m[j]);
     }
     __syncthreads();  // wtot is rewritten by the next pass

@@ -22,6 +22,25 @@ __device__ unsigned long long g_trace[256];
 
 constexpr int kStatusActive = 127;  // internal: sample still iterating
 
+// Checked build (-DRBNS_CHECKED, build/librbns_checked.so; compute-sanitizer is not available on this pool):
+// bounds and protocol checks on the hot kernels' global and shared indexing.  A failed check records its
+// source line (first one wins) and counts; rbns_debug_checks() reads the counters of every translation unit.
+#ifdef RBNS_CHECKED
+static __device__ int g_chk_line;
+static __device__ unsigned long long g_chk_count;
+#define RBNS_CHECK(cond)                              \
+  do {                                                \
+    if (!(cond)) {                                    \
+      atomicCAS(&::rbns::g_chk_line, 0, __LINE__);    \
+      atomicAdd(&::rbns::g_chk_count, 1ull);          \
+    }                                                 \
+  } while (0)
+#else
+#define RBNS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 __device__ __forceinline__ double ipow(double x, int n) {
   double r = 1.0;
   for (int i = 0; i < n; ++i) r = r * x;

@@ -49,6 +49,7 @@ struct ContractParams {
   double* out;            // [n][ldo]
   int64_t ldo;
   const double* wts;      // [B][Qb + Ql] precomputed weights (eval_weights), indexed by sample id; NULL = evaluate
+  int64_t B;              // samples of the call (sample ids < B; checked builds), 0 = n
 };
 
 #ifndef RBNS_BN
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
     const int i = tile0 + b;
     if (i < p.n) {
       const int id = p.act ? p.act[i] : i;
+      RBNS_CHECK(id >= 0 && id < (p.B > 0 ? p.B : p.n));
       if (p.wts) {
         const double* w = p.wts + int64_t(id) * (p.Qb + p.Ql);
         for (int q = 0; q < p.Qb; ++q) thS[q * BM + b] = w[q];
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       const int i = tile0 + sb0 + mi * 8 + g;
       if (i < p.n) {
         double* o = p.out + int64_t(i) * p.ldo + int64_t(rt) * BN + rb0 + 2 * t;
+        RBNS_CHECK(int64_t(rt) * BN + rb0 + 2 * t + (NI - 1) * 8 + 1 < p.ldo);
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni)
           *reinterpret_cast<double2*>(o + ni * 8) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);

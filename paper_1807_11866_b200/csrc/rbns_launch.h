@@ -19,6 +19,9 @@ cudaError_t newton_prepare(int N);
 // launches the Newton-update kernel(s) for p on st; *launches receives the number of kernels launched
 cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* launches);
 
+// checked builds (-DRBNS_CHECKED): this translation unit's failed-check counters (first source line, count)
+int newton_debug_checks(int* line, unsigned long long* count);
+
 // records msg as the calling thread's rbns_last_error_message() and returns code (entry points outside rbns.cu)
 int set_last_error(int code, const std::string& msg);
 

@@ -216,6 +216,18 @@ cudaError_t launch_newton_update(const NewtonParams& p, cudaStream_t st, int* la
 
 }  // namespace rbns
 
+int rbns::newton_debug_checks(int* line, unsigned long long* count) {
+#ifdef RBNS_CHECKED
+  if (cudaMemcpyFromSymbol(line, rbns::g_chk_line, sizeof(int)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(count, rbns::g_chk_count, sizeof(unsigned long long)) != cudaSuccess)
+    return 2;
+#else
+  *line = 0;
+  *count = 0;
+#endif
+  return 0;
+}
+
 #ifdef RBNS_TGH_DUMP
 extern "C" int rbns_debug_tgh(double* out) {
   return cudaMemcpyFromSymbol(out, rbns::g_tgh_dump, sizeof(double) * 4 * 256) == cudaSuccess ? 0 : 2;

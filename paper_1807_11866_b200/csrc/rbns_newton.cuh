@@ -43,6 +43,7 @@ struct NewtonParams {
   const double* wf;            // [B][Qf + G] precomputed residual weights (eval_load_weights), or NULL
   int32_t jl;                  // layout of the J block (jidx, rbns_common.cuh): 0 row-major, 1 tile layout
   int32_t num_sms;             // SMs of the model's device (persistent / subset grids)
+  int64_t B;                   // samples of the call (sample ids < B; checked builds)
 };
 
 // CTA → chunk position (and whether this CTA has work) for the exact kernels' optional subset launch

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(TGR * TGC, (TGR * TGC <= 128 ? 2 : 1)) newton_
   for (int j = blockIdx.x; j < n; j += gridDim.x) {
     const int i_s = p.sub ? p.sub[j] : j;
     const int b = p.act[i_s];
+    RBNS_CHECK(i_s >= 0 && i_s < p.n && b >= 0 && (p.B == 0 || b < p.B));
     double a[RS][CS];
     gj_load_system<TGR, TGC, RS, CS>(p, i_s, b, a, sh);
     bool sing = false;

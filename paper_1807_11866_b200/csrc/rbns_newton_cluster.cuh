@@ -239,6 +239,7 @@ __device__ __forceinline__ void gjc_sample(const NewtonParams& p, const int i_s,
   constexpr int NW = NT / 32;
   cg::cluster_group cluster = cg::this_cluster();
   const int b = p.act[i_s];
+    RBNS_CHECK(i_s >= 0 && i_s < p.n && b >= 0 && (p.B == 0 || b < p.B));
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
   const int rhs_rank = (N % (2 * TGC)) / TGC, rhs_tc = N % TGC, rhs_slot = N / (2 * TGC);

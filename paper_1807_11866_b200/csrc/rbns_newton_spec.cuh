@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(TGR * TGC, MINB) newton_gjs_kernel(const Newto
   const int i_s = blockIdx.x;
   if (i_s >= p.n) return;
   const int b = p.act[i_s];
+    RBNS_CHECK(i_s >= 0 && i_s < p.n && b >= 0 && (p.B == 0 || b < p.B));
   const int tid = threadIdx.x, tc = tid / TGR, tr = tid % TGR;
   const int N = p.N;
   for (int i = tid; i < NR; i += NT) {

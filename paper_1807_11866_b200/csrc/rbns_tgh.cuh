@@ -224,10 +224,12 @@ __global__ void __launch_bounds__(NW * 32, tgh_min_blocks<NW, REG>()) newton_tgh
   uint32_t phase = 0;
   int pc0 = 0;
   const uint32_t jbytes = uint32_t(((int64_t(N) * N + int64_t(p.G) * N) * 8 + 15) & ~int64_t(15));
+  RBNS_CHECK(int64_t(jbytes) <= p.ldj * 8 && N <= NR && N > 8 * (RT - 1));
 
 #pragma unroll 1
   for (int i_s = blockIdx.x; i_s < p.n; i_s += gridDim.x) {
     const int b = p.act[i_s];
+    RBNS_CHECK(i_s >= 0 && i_s < p.n && b >= 0 && (p.B == 0 || b < p.B));
     const double* Jb = p.J + int64_t(i_s) * p.ldj;
     if (tid == 0) {
       if constexpr (kFull) {  // shared J tiles by the TMA engine (contiguous 8N-double column-tile blocks)
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(NW * 32, tgh_min_blocks<NW, REG>()) newton_tgh
           if (!((REG >> s) & 1))
             for (int w = 0; w < NW; ++w) {
               const int j = 1 + s * NW + w;
+              RBNS_CHECK(j >= CT - 1 || int64_t(8 * j) * N + int64_t(RT) * 64 <= int64_t(N) * N);
               if (j < CT - 1)
                 bulk_g2s(&sh.T[tgh_sidx<CT, NW, REG>(s, w)][0][0], Jb + int64_t(8 * j) * N, kTileBytes, &sh.bar, pol);
             }
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(NW * 32, tgh_min_blocks<NW, REG>()) newton_tgh
           }
         } else if (j < CT && cr > 0) {
           const double* tb = Jb + int64_t(8 * j) * N + 8 * i * cr;
+          RBNS_CHECK(int64_t(8 * j) * N + 8 * i * cr + (cr - 1) * rr + rr <= int64_t(N) * N);
           if (cr == 8 && rr == 8) {
             const double2 v = __ldcs(reinterpret_cast<const double2*>(tb) + lane);
             v0 = v.x;

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>()) newton_tgj_kern
     fence_barrier_init();
   }
   __syncthreads();
+  RBNS_CHECK(int64_t(jbytes) <= p.ldj * 8);  // the staging buffer holds ldj doubles
   auto issue = [&](int is) {  // thread 0: stage sample is's J block
     const uint64_t pol = l2_policy_evict_first();
     mbar_arrive_expect_tx(&sh.bar, jbytes);
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>()) newton_tgj_kern
 #pragma unroll 1
   for (int i_s = blockIdx.x; i_s < p.n; i_s += gridDim.x) {
     const int b = p.act[i_s];
+    RBNS_CHECK(i_s >= 0 && i_s < p.n && b >= 0 && (p.B == 0 || b < p.B));
     const int nxt_s = i_s + int(gridDim.x);
     // J-independent work first, while the block may still be in flight: pivot-order hint, f(μ), weights, u
     bool ident = true;
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>()) newton_tgj_kern
         double v0 = 0.0, v1 = 0.0;
         if (j < CT && cr > 0) {
           const double* tb = jst + int64_t(8 * j) * N + 8 * i * cr;
+          RBNS_CHECK(int64_t(8 * j) * N + 8 * i * cr + (cr - 1) * rr + rr <= int64_t(N) * N);
           if (cr == 8 && rr == 8) {
             const double2 v = *reinterpret_cast<const double2*>(tb + 2 * lane);
             v0 = v.x;
