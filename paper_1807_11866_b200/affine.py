@@ -98,6 +98,36 @@ def family(name: str) -> List[ThetaTerm]:
     raise ValueError(f"unknown theta family {name!r}")
 
 
+def dependence(terms: Sequence[ThetaTerm], samples: int = 64, seed: int = 0, rtol: float = 1e-12):
+    """Linear dependence among the coefficient functions of one family: returns (basis, coef) with basis the
+    indices of a maximal independent subset (first occurrences kept, in order) and coef[q] the exact-to-rounding
+    coefficients expressing θ_q in that basis, θ_q(μ) = Σ_i coef[q, i] θ_basis[i](μ) for every μ.
+
+    The functions are sampled at random μ (α ∈ [−π, π], μ₁ ∈ [0.5, 2]: any point set in general position
+    determines a dependence among these analytic functions); a term joins the basis when its least-squares
+    residual against the current basis exceeds rtol relative.  E.g. BASELINE's trig7 list (1, cos α, sin α, cos²α,
+    sin²α, sin α cos α, cos 2α) spans only 5 functions: sin²α = 1 − cos²α, cos 2α = 2cos²α − 1."""
+    terms = list(terms)
+    rng = np.random.default_rng(seed)
+    mu = np.stack([rng.uniform(-np.pi, np.pi, samples), rng.uniform(0.5, 2.0, samples)], axis=1)
+    Th = evaluate_weights(terms, mu)
+    basis: List[int] = []
+    coef = np.zeros((len(terms), len(terms)))
+    for q in range(len(terms)):
+        col = Th[:, q]
+        if basis:
+            c, *_ = np.linalg.lstsq(Th[:, basis], col, rcond=None)
+            snap = np.round(c * 2.0 ** 20) / 2.0 ** 20  # dyadic relations (±1, 2, ½ …) exactly
+            c = np.where(np.abs(c - snap) <= 1e-12 * np.maximum(1.0, np.abs(c)), snap, c)
+            res = np.linalg.norm(Th[:, basis] @ c - col)
+            if res <= rtol * max(np.linalg.norm(col), 1e-300):
+                coef[q, :len(basis)] = c
+                continue
+        basis.append(q)
+        coef[q, len(basis) - 1] = 1.0
+    return basis, coef[:, :len(basis)]
+
+
 def monomials(powers: Iterable[tuple], scales: Iterable[float] | None = None) -> List[ThetaTerm]:
     """The paper's exact monomial family scale·αᵏ·Reᵐ from (k, m) pairs."""
     powers = list(powers)

@@ -148,3 +148,38 @@ class ReducedModel:
     @property
     def theta_list(self) -> List[ThetaTerm]:
         return list(self.theta)
+
+    def compress_affine(self) -> "ReducedModel":
+        """The same model with linearly dependent coefficient functions merged, family by family (an exact
+        algebraic rewrite of the affine sums Σ_q θ_q(μ) X_q; round-off aside the reduced
+        residual and Jacobian are unchanged): each family keeps a maximal independent subset of its own
+        descriptors (``affine.dependence``) and X'_i = Σ_q coef[q, i] X_q.  BASELINE's trig7 family (configs 1, 2
+        and 4) has 5 independent functions among its 7, so the convective contraction does 5/7 of the work.
+        Returns self when nothing is dependent."""
+        from .affine import dependence
+
+        arrays = {"linear": self.A, "quadratic": self.C, "load": self.f, "coupling": self.Bq}
+        out, changed, kept = {}, False, {}
+        for fam in FAMILIES:
+            terms = list(getattr(self, f"theta_{fam}"))
+            X = arrays[fam]
+            if X is None or not terms:
+                out[fam] = (X, terms)
+                continue
+            basis, coef = dependence(terms)
+            kept[fam] = [len(terms), len(basis)]
+            if len(basis) == len(terms):
+                out[fam] = (X, terms)
+                continue
+            changed = True
+            Xf = X.reshape(X.shape[0], -1)
+            out[fam] = ((coef.T @ Xf).reshape((len(basis),) + X.shape[1:]), [terms[i] for i in basis])
+        if not changed:
+            return self
+        from dataclasses import replace
+
+        return replace(self, A=out["linear"][0], C=out["quadratic"][0], f=out["load"][0],
+                       Bq=out["coupling"][0] if self.Bq is not None else None, theta=(),
+                       theta_linear=out["linear"][1], theta_quadratic=out["quadratic"][1],
+                       theta_load=out["load"][1], theta_coupling=out["coupling"][1] if self.Bq is not None else None,
+                       name=f"{self.name}-compressed", meta=dict(self.meta, affine_compressed=kept))
