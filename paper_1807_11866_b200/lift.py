@@ -57,6 +57,6 @@ def lifted_error(U, U_ref, G: Optional[np.ndarray] = None, device="cuda"):
     if G is None:
         num, den = (D * D).sum(1), (R * R).sum(1)
     else:
-        Gt = torch.as_tensor(G, dtype=torch.float64, device=device)
+        Gt = torch.as_tensor(np.array(G, dtype=np.float64), dtype=torch.float64, device=device)
         num, den = (D * (D @ Gt)).sum(1), (R * (R @ Gt)).sum(1)
     return torch.sqrt(num / den)
