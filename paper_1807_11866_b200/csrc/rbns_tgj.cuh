@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>()) newton_tgj_kern
       continue;
     }
 
+    TGJ_TR(9);
     // ---- owned column tiles j = 1 + warp + NW·jj from the staging buffer ----
     double acc[JJ][RT][2];
 #pragma unroll

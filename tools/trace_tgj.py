@@ -15,7 +15,7 @@ with online.DeviceModel(m, 0) as dm:
     buf = (ctypes.c_ulonglong * 256)()
     _native.load().rbns_debug_trace(buf, 256)
 names = {0: "sample start", 1: "J landed", 2: "rhs + M0 ready", 3: "staging consumed", 4: "panel 0 published",
-         250: "sample done", 5: "tiles loaded", 6: "row sums reduced", 7: "row-sum barrier", 8: "rhs computed"}
+         250: "sample done", 5: "tiles loaded", 6: "row sums reduced", 7: "row-sum barrier", 8: "rhs computed", 9: "hint checked"}
 for P in range(16):
     names[192 + P] = f"P{P}: owner starts invert"; names[208 + P] = f"P{P}: invert done"
     names[224 + P] = f"P{P}: published"
