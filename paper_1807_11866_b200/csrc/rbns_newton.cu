@@ -1,7 +1,7 @@
 // rbns_newton.cu — instantiation + dispatch of the Newton-update kernels; kept in its own translation unit so
 // the instantiations compile in parallel with the rest of the library.
-//   tiled Gauss–Jordan (rbns_tgj.cuh)      default where a shape is instantiated (N = 49..55, 89..103)
-//   speculative rank-1 (rbns_newton_spec)   other N ≤ 127, hinted pivot order, misses → exact kernel
+//   tiled Gauss–Jordan (rbns_tgj.cuh)      default for 32 < N ≤ 103 (shapes: rbns_tgj_shapes_*.cu)
+//   speculative rank-1 (rbns_newton_spec)   N ≤ 32 and 103 < N ≤ 127, hinted pivot order, misses → exact kernel
 //   exact rank-1 (rbns_newton2.cuh)         full partial-pivot search: every miss of the speculative kernels
 //   hybrid tiled Gauss–Jordan (rbns_tgh.cuh) N = 200 (config 3): one CTA per sample, registers + shared memory
 //   2-CTA cluster (rbns_newton_cluster)     other 127 < N ≤ 207, and the exact path of the hybrid kernel
@@ -17,6 +17,7 @@
 #include "rbns_newton_cluster.cuh"
 #include "rbns_tgj.cuh"
 #include "rbns_tgh.cuh"
+#include "rbns_tiled_plan.h"
 
 namespace rbns {
 
@@ -61,23 +62,6 @@ const Shape* plan(int N) {
   return nullptr;
 }
 
-// tiled Gauss–Jordan kernel (rbns_tgj.cuh): RT = ⌈N/8⌉ row tiles, CT = ⌈(N+1)/8⌉ column tiles, NW warps
-struct TShape {
-  int rt, ct, nw;
-  NewtonKernel kern;
-  size_t base;  // shared memory before the J staging buffer
-  int minb;     // resident CTAs per SM (persistent grid = minb × SMs)
-};
-#define RBNS_TS(R_, C_, W_) \
-  {R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>(), tgj_min_blocks<R_>()}
-const TShape kTShapes[] = {
-    RBNS_TS(13, 13, 4),  // 96 < N ≤ 103 (config 2 / 4: N = 100)
-    RBNS_TS(12, 13, 4),  // N = 96
-    RBNS_TS(12, 12, 4),  // 88 < N < 96
-    RBNS_TS(7, 7, 4),    // 48 < N ≤ 55 (config 1: N = 50)
-};
-#undef RBNS_TS
-
 const TShape* tplan(int N) {
   static const bool off = [] {  // any RBNS_NEWTON value other than "tgj" selects the earlier kernels
     const char* v = std::getenv("RBNS_NEWTON");
@@ -85,8 +69,10 @@ const TShape* tplan(int N) {
   }();
   if (off || N <= 8) return nullptr;
   const int rt = (N + 7) / 8, ct = (N + 8) / 8;
-  for (const TShape& s : kTShapes)
-    if (s.rt == rt && s.ct == ct) return &s;
+  for (int i = 0; i < kTShapesA_n; ++i)
+    if (kTShapesA[i].rt == rt && kTShapesA[i].ct == ct) return &kTShapesA[i];
+  for (int i = 0; i < kTShapesB_n; ++i)
+    if (kTShapesB[i].rt == rt && kTShapesB[i].ct == ct) return &kTShapesB[i];
   return nullptr;
 }
 
