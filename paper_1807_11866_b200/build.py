@@ -43,7 +43,10 @@ def build(verbose: bool = False, force: bool = False, out: Path = OUT, extra=())
 
     def compile_one(src: Path) -> Path:
         obj = obj_dir / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
+        flags = NVCC_FLAGS
+        if "_shapes_" in src.name:  # coverage instantiations: no line tables (3x the object size); the
+            flags = [f for f in NVCC_FLAGS if f != "-lineinfo"]  # profiled shapes are in rbns_tiled_main.cu
+        cmd = [nvcc, *flags, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,15 +1,16 @@
 // rbns_newton.cu — instantiation + dispatch of the Newton-update kernels; kept in its own translation unit so
 // the instantiations compile in parallel with the rest of the library.
 //   tiled Gauss–Jordan (rbns_tgj.cuh)      default for 32 < N ≤ 103 (shapes: rbns_tgj_shapes_*.cu)
-//   speculative rank-1 (rbns_newton_spec)   N ≤ 32 and 103 < N ≤ 127, hinted pivot order, misses → exact kernel
+//   speculative rank-1 (rbns_newton_spec)   N ≤ 32, hinted pivot order, misses → exact kernel
 //   exact rank-1 (rbns_newton2.cuh)         full partial-pivot search: every miss of the speculative kernels
-//   hybrid tiled Gauss–Jordan (rbns_tgh.cuh) N = 200 (config 3): one CTA per sample, registers + shared memory
-//   2-CTA cluster (rbns_newton_cluster)     other 127 < N ≤ 207, and the exact path of the hybrid kernel
+//   hybrid tiled Gauss–Jordan (rbns_tgh.cuh) 103 < N ≤ 200: one CTA per sample, registers + shared memory
+//   2-CTA cluster (rbns_newton_cluster)     200 < N ≤ 207, and the exact path of the hybrid kernel
 // RBNS_NEWTON=gjs forces the speculative rank-1 kernels, RBNS_NEWTON=gj2 the exact one (parity-tested).
 #include "rbns_launch.h"
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "rbns_newton.cuh"
 #include "rbns_newton2.cuh"
@@ -69,6 +70,8 @@ const TShape* tplan(int N) {
   }();
   if (off || N <= 8) return nullptr;
   const int rt = (N + 7) / 8, ct = (N + 8) / 8;
+  for (int i = 0; i < kTShapesMain_n; ++i)
+    if (kTShapesMain[i].rt == rt && kTShapesMain[i].ct == ct) return &kTShapesMain[i];
   for (int i = 0; i < kTShapesA_n; ++i)
     if (kTShapesA[i].rt == rt && kTShapesA[i].ct == ct) return &kTShapesA[i];
   for (int i = 0; i < kTShapesB_n; ++i)
@@ -76,24 +79,6 @@ const TShape* tplan(int N) {
   return nullptr;
 }
 
-// hybrid register/shared-memory tiled kernel (rbns_tgh.cuh): RT row tiles, CT column tiles, NW warps, REG =
-// register slots; persistent grid of minb CTAs per SM
-struct HShape {
-  int rt, ct, nw;
-  NewtonKernel kern;
-  size_t smem;
-  int minb;
-  bool test_only;  // instantiated for the tests (RBNS_NEWTON=tgh), not the default for its N
-};
-#define RBNS_HS(R_, C_, W_, G_, T_) \
-  {R_, C_, W_, newton_tgh_kernel<R_, C_, W_, G_>, tgh_smem_bytes<R_, C_, W_, G_>(), tgh_min_blocks<W_, G_>(), T_}
-const HShape kHShapes[] = {
-    RBNS_HS(25, 26, 12, 2, false),  // N = 200 (config 3): 12 register + 13 shared column tiles, 1 CTA/SM
-    RBNS_HS(13, 13, 4, 6, true),    // 96 < N ≤ 103: 2 register + 1 shared tile per warp, 3 CTAs/SM
-    RBNS_HS(7, 8, 3, 2, true),      // N = 56  (tests)
-    RBNS_HS(13, 14, 6, 2, true),    // N = 104 (tests)
-};
-#undef RBNS_HS
 const HShape* hplan(int N) {
   static const int mode = [] {  // 0: default (config-3 shape), 1: off, 2: every instantiated shape
     const char* v = std::getenv("RBNS_NEWTON");
@@ -102,8 +87,10 @@ const HShape* hplan(int N) {
   }();
   if (mode == 1 || N <= 8) return nullptr;
   const int rt = (N + 7) / 8, ct = (N + 8) / 8;
-  for (const HShape& s : kHShapes)
-    if (s.rt == rt && s.ct == ct && (mode == 2 || !s.test_only)) return &s;
+  for (const auto& [tab, cnt] : {std::pair{kHShapesMain, kHShapesMain_n}, std::pair{kHShapesA, kHShapesA_n},
+                                  std::pair{kHShapesB, kHShapesB_n}, std::pair{kHShapesC, kHShapesC_n}})
+    for (int i = 0; i < cnt; ++i)
+      if (tab[i].rt == rt && tab[i].ct == ct && (mode == 2 || !tab[i].test_only)) return &tab[i];
   return nullptr;
 }
 }  // namespace

@@ -78,9 +78,10 @@ __host__ __device__ constexpr size_t tgh_smem_bytes() {
   return (sizeof(TGHShared<RT, CT, NW, REG>) + 127) & ~size_t(127);
 }
 
-// resident CTAs per SM: as many as the register file holds (≤ 3), one for the 12-warp config-3 shape
+// resident CTAs per SM the register file is budgeted for: 1 (≥ 8 warps: N > 127), 2 (5–7 warps: 103 < N ≤ 127),
+// 3 (≤ 4 warps: the N ≤ 103 alternate)
 template <int NW, int REG>
-constexpr int tgh_min_blocks() { return NW >= 8 ? 1 : 3; }
+constexpr int tgh_min_blocks() { return NW >= 8 ? 1 : NW >= 5 ? 2 : 3; }
 
 // Row tile P of a register column tile by a chain of selects (static register indices, 4 live registers).
 template <int RT>

@@ -8,7 +8,7 @@
 namespace rbns {
 const TShape kTShapesA[] = {
     RBNS_TS(5, 5, 4), RBNS_TS(5, 6, 4), RBNS_TS(6, 6, 4), RBNS_TS(6, 7, 4),
-    RBNS_TS(7, 7, 4), RBNS_TS(7, 8, 4), RBNS_TS(8, 8, 4), RBNS_TS(8, 9, 4),
+    RBNS_TS(7, 8, 4), RBNS_TS(8, 8, 4), RBNS_TS(8, 9, 4),
 };
 const int kTShapesA_n = int(sizeof(kTShapesA) / sizeof(kTShapesA[0]));
 }  // namespace rbns

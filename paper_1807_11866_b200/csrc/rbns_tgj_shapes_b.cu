@@ -6,7 +6,7 @@
 namespace rbns {
 const TShape kTShapesB[] = {
     RBNS_TS(9, 9, 4),   RBNS_TS(9, 10, 4),  RBNS_TS(10, 10, 4), RBNS_TS(10, 11, 4), RBNS_TS(11, 11, 4),
-    RBNS_TS(11, 12, 4), RBNS_TS(12, 12, 4), RBNS_TS(12, 13, 4), RBNS_TS(13, 13, 4),
+    RBNS_TS(11, 12, 4), RBNS_TS(12, 12, 4), RBNS_TS(12, 13, 4),
 };
 const int kTShapesB_n = int(sizeof(kTShapesB) / sizeof(kTShapesB[0]));
 }  // namespace rbns

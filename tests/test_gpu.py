@@ -600,6 +600,21 @@ def test_hybrid_kernel_test_shapes():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
 
+@pytest.mark.parametrize("n", [33, 40, 64, 80, 104, 111, 120, 127, 128, 150, 175, 192, 199])
+def test_tiled_kernel_shapes_default_path(n):
+    """Every instantiated tiled shape family on the default dispatch: register kernel (32 < N ≤ 103), hybrid
+    register/shared kernel with 5 warps (103 < N ≤ 127) and with 12 warps (127 < N < 200), partial and full tiles,
+    against the oracle."""
+    rng_seed = n
+    model = synthetic.make_model(n, 3, "trig3", seed=rng_seed)
+    mu = synthetic.make_mu(64, 50.0, seed=rng_seed)
+    with online.DeviceModel(model, 0) as dm:
+        u, _, it, st, _, stats = device_solve(dm, mu)
+    ur, itr, str_, _ = oracle.solve_batch(model, mu)
+    assert np.all(st == 0) and np.all(str_ == 0)
+    assert (np.abs(u - ur).max(axis=1) / np.abs(ur).max(axis=1)).max() <= REL
+    check_counts(model, mu, it, itr)
+
 def test_unsupported_size_fails_loudly():
     """N beyond the register/cluster Newton kernels (207) is rejected at model creation, not computed wrong."""
     n = 208
