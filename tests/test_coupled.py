@@ -103,3 +103,28 @@ def test_unstabilised_device_singular():
     assert np.all(st == oracle.SINGULAR_SYSTEM) and np.all(it == 1)
     with pytest.raises(SingularSystemError):
         solve_coupled(cm, synthetic.make_lifted_mu(1)[0])
+
+
+@pytest.mark.gpu
+def test_timing_study_block_vs_coupled_scaling():
+    """SPEC.md:630-638 timing_study examples on the device: block < coupled-3M at every M, and the coupled-3M time
+    grows ≈ cubically in M (fitted exponent in [2.2, 3.5] over M ∈ {10, 20, 30, 50}; the dense LU of the
+    (3M)-sized saddle system dominates)."""
+    import torch
+
+    from paper_1807_11866_b200 import online, study
+    from paper_1807_11866_b200.coupled import solve_coupled_batch
+
+    ms, tc = (10, 20, 30, 50), []
+    for m in ms:
+        cm, blk = synthetic.make_coupled_model(m, 12)
+        mu = synthetic.make_lifted_mu(4096, seed=3)
+        with online.DeviceModel(blk, 0) as dm:
+            t = study.timing_study({"block": lambda x: dm.solve(x, pressure=False),
+                                    "coupled": lambda x: solve_coupled_batch(cm, x.cpu().numpy())}, mu)
+        assert t["block"] < t["coupled"], (m, t)
+        tc.append(t["coupled"])
+        torch.cuda.synchronize()
+    slope = study.loglog_slope(ms, tc)
+    print(f"coupled-3M ms/query {[round(x, 5) for x in tc]}, fitted exponent {slope:.2f}")
+    assert 2.2 <= slope <= 3.5, slope
