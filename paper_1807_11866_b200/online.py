@@ -11,6 +11,8 @@ Public API (names and meaning follow the SPEC):
 * :func:`solve_block` (rm, μ) → ReducedSolution — SPEC.md:520-528; raises SingularSystemError for
   SINGULAR_SYSTEM / SINGULAR_RECOVERY (SPEC.md:514, :524); NON_CONVERGED is reported, not raised.
 * :func:`solve_block_batch` (rm, μ[B,2]) → :class:`BatchSolution` — the batch sweep API.
+* :func:`query` (model, μ, solver) → :class:`ReducedSolution` — the query API over the block,
+  combined (:func:`solve_combined`) and coupled solvers.
 * :func:`reduced_operator` (rm, μ, η) → (residual, Jacobian) — SPEC.md:500-508.
 * :func:`recover_pressure` — a-posteriori recovery alone for given velocities (SPEC.md:523 step 2).
 * :func:`reconstruct_pressure` (rm, u_coeffs) → p_coeffs — the combined scheme's reconstruction from the
@@ -396,6 +398,52 @@ def solve_block(rm: ReducedModel, mu, tol: float = DEFAULT_TOL, max_iter: int = 
         mu=(float(mu_np[0]), float(mu_np[1])), u_coeffs=res["u"][0].copy(), s_coeffs=np.zeros(rm.n),
         p_coeffs=None if res["p"] is None else res["p"][0].copy(), newton_iters=int(res["iters"][0]),
         wall_time=wt, converged=st == CONVERGED, status=st, last_update=float(res["last_update"][0]))
+
+
+def solve_combined(rm: ReducedModel, mu, tol: float = DEFAULT_TOL, max_iter: int = DEFAULT_MAX_ITER,
+                   device: int = 0) -> ReducedSolution:
+    """Single query of the combined scheme: the block velocity solve without
+    the recovery solve, then p = P_att u from the model's attached pressure modes."""
+    if rm.P_att is None:
+        raise RbflowError("solve_combined: the reduced model carries no attached pressure modes "
+                          "(built without the combined flag, SPEC.md:449)")
+    dm = device_model(rm, device)
+    mu_np = np.asarray(mu, dtype=np.float64).reshape(2)
+    t0 = time.perf_counter()
+    res = dm.solve_host(mu_np.reshape(1, 2), tol=tol, max_iter=max_iter, pressure=False)
+    t1 = time.perf_counter()
+    st = int(res["status"][0])
+    if st == SINGULAR_SYSTEM:
+        raise SingularSystemError(f"SINGULAR_SYSTEM at mu={tuple(mu_np)} after {int(res['iters'][0])} iterations")
+    p = reconstruct_pressure(rm, res["u"][0], device)
+    wt = _phase_times(res["stats"])
+    wt["recovery"] = time.perf_counter() - t1
+    wt["total"] = time.perf_counter() - t0
+    return ReducedSolution(
+        mu=(float(mu_np[0]), float(mu_np[1])), u_coeffs=res["u"][0].copy(), s_coeffs=np.zeros(rm.n),
+        p_coeffs=p, newton_iters=int(res["iters"][0]), wall_time=wt, converged=st == CONVERGED, status=st,
+        last_update=float(res["last_update"][0]))
+
+
+SOLVERS = ("block", "combined", "coupled")
+
+
+def query(model, mu, solver: str = "block", device: int = 0, **kw) -> ReducedSolution:
+    """The Query API: (μ, solver kind) → ReducedSolution.  ``solver``: "block" (velocity-only
+    Newton + a-posteriori pressure recovery), "combined" (block velocity + reconstruction from the
+    attached modes) or "coupled" (the stabilised coupled-3M system; ``model`` is then
+    a ``coupled.CoupledModel``)."""
+    if solver == "block":
+        return solve_block(model, mu, device=device, **kw)
+    if solver == "combined":
+        return solve_combined(model, mu, device=device, **kw)
+    if solver == "coupled":
+        from .coupled import CoupledModel, solve_coupled
+
+        if not isinstance(model, CoupledModel):
+            raise TypeError("solver='coupled' needs a coupled.CoupledModel")
+        return solve_coupled(model, mu, device=device, **kw)
+    raise ValueError(f"solver={solver!r}: use one of {SOLVERS}")
 
 
 def reduced_operator(rm: ReducedModel, mu, eta, device: int = 0) -> Tuple[np.ndarray, np.ndarray]:

@@ -622,3 +622,28 @@ def test_unsupported_size_fails_loudly():
                          theta=[affine.ThetaTerm(affine.CONST)])
     with pytest.raises(NativeError, match="exceeds"):
         online.DeviceModel(model, 0)
+
+
+def test_query_api_solver_kinds():
+    """SPEC.md:566 Query API: (μ, solver kind) → ReducedSolution for the block, combined and coupled solvers;
+    block and combined share the velocity, combined pressure = P_att u, coupled velocity within 1e-8 of block."""
+    from paper_1807_11866_b200.coupled import solve_coupled
+
+    model = synthetic.config_model(4, attached=True)
+    mu = synthetic.config_mu(4, 2)[1]
+    b = online.query(model, mu, "block")
+    c = online.query(model, mu, "combined")
+    assert b.converged and c.converged and b.newton_iters == c.newton_iters
+    np.testing.assert_array_equal(b.u_coeffs, c.u_coeffs)
+    np.testing.assert_allclose(c.p_coeffs, oracle.reconstruct_pressure(model, b.u_coeffs[None])[0], rtol=1e-12,
+                               atol=1e-14)
+    assert b.p_coeffs is not None and not np.array_equal(b.p_coeffs, c.p_coeffs)  # recovery ≠ reconstruction
+    cm, blk = synthetic.make_coupled_model(10, 2)
+    mu2 = synthetic.make_lifted_mu(1, seed=4)[0]
+    q = online.query(cm, mu2, "coupled")
+    r = online.query(blk, mu2, "block")
+    assert np.abs(q.u_coeffs - r.u_coeffs).max() <= 1e-8 * np.abs(r.u_coeffs).max()
+    with pytest.raises(ValueError):
+        online.query(model, mu, "nonsense")
+    with pytest.raises(TypeError):
+        online.query(model, mu, "coupled")
