@@ -183,3 +183,25 @@ def test_lifted_reduced_operator_device(dmodels):
     for b in range(16):
         Rr, Jr = oracle.reduced_operator(m, mu[b], eta[b])
         assert _rel(R[b], Rr) <= 1e-12 and _rel(J[b], Jr) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_weight_consistency_phi0_device(dmodels):
+    """SPEC.md:508 weight consistency: the residual (and Jacobian) at μ = (φ, u∞) = (0, 1) equals that of the
+    model restricted to its φ⁰ terms (every other monomial vanishes there), to 1e-13 — on the device."""
+    from paper_1807_11866_b200 import online
+
+    m = lifted("lifted_small")
+    keep = {fam: [i for i, t in enumerate(getattr(m, f"theta_{fam}")) if t.k == 0]
+            for fam in ("linear", "quadratic", "load")}
+    m0 = ReducedModel(A=m.A[keep["linear"]], C=m.C[keep["quadratic"]], f=m.f[keep["load"]],
+                      theta_linear=[m.theta_linear[i] for i in keep["linear"]],
+                      theta_quadratic=[m.theta_quadratic[i] for i in keep["quadratic"]],
+                      theta_load=[m.theta_load[i] for i in keep["load"]], nu_linear=m.nu_linear)
+    mu = np.array([[0.0, 1.0]] * 4)
+    eta = np.random.default_rng(5).standard_normal((4, m.n)) * 20
+    R, J = dmodels("lifted_small").reduced_operator(mu, eta)
+    with online.DeviceModel(m0, 0) as dm0:
+        R0, J0 = dm0.reduced_operator(mu, eta)
+    R, J, R0, J0 = (x.cpu().numpy() for x in (R, J, R0, J0))
+    assert _rel(R, R0) <= 1e-13 and _rel(J, J0) <= 1e-13
