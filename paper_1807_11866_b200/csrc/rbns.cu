@@ -669,7 +669,7 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
     op.Qb = qb;
     op.Ql = ql;
     op.kalloc = qb * m->Ne + (ql + 3) / 4 * 4;
-    op.nchunks = (op.kalloc + 7) / 8;
+    op.nchunks = (op.kalloc + 4 * kKSub - 1) / (4 * kKSub);
     op.nsub = op.kalloc / 4;
 #ifndef RBNS_STAGES
 #define RBNS_STAGES 16

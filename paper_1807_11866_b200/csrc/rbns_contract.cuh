@@ -39,7 +39,7 @@ struct ContractParams {
   int32_t nu_lin;         // affine columns carry ν = 1/μ₁
   const rbns_theta_term* thb;  // [Qb] block descriptors (device)
   const rbns_theta_term* thl;  // [Ql] affine-column descriptors (device)
-  int32_t nchunks;        // TMA stages per row tile (8 κ each)
+  int32_t nchunks;        // TMA stages per row tile (4·kKSub κ each)
   int32_t nsub;           // k4 sub-steps per row tile (= K / 4)
   int32_t sub_begin;      // first k4 sub-step (Qb·Ne/4 at u = 0: only the affine block is non-zero)
   int32_t row_tiles;      // ceil(R / BN)
@@ -61,14 +61,17 @@ struct ContractParams {
 #ifndef RBNS_WM
 #define RBNS_WM 2
 #endif
-constexpr int kBM = 64, kBN = RBNS_BN, kWM = RBNS_WM, kWN = RBNS_WN;
+#ifndef RBNS_KSUB
+#define RBNS_KSUB 2  // 4-κ k-steps per TMA stage (one full/empty mbarrier round trip per stage)
+#endif
+constexpr int kBM = 64, kBN = RBNS_BN, kWM = RBNS_WM, kWN = RBNS_WN, kKSub = RBNS_KSUB;
 constexpr int kContractThreads = (kWM * kWN + 1) * 32;
 
 // u-tile row stride ≡ 4 (mod 16) doubles: the 4 rows a half-warp touches land in distinct 32-byte bank groups
 __host__ __device__ inline int contract_ldu(int ne) { return ne + ((4 - ne % 16) + 16) % 16; }
 
 __host__ inline size_t contract_smem_bytes(int stages, int ldu, int qb, int ql) {
-  return size_t(stages) * 2 * kBN * 4 * sizeof(double) + size_t(kBM) * ldu * sizeof(double) +
+  return size_t(stages) * kKSub * kBN * 4 * sizeof(double) + size_t(kBM) * ldu * sizeof(double) +
          size_t(qb + ql) * kBM * sizeof(double) + 2 * size_t(stages) * sizeof(uint64_t);
 }
 
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
   constexpr int NCW = WM * WN;
   constexpr int TM = BM / WM, TN = BN / WN;
   constexpr int MI = TM / 8, NI = TN / 8;
-  constexpr int STAGE = 2 * BN * 4;  // doubles per stage: two [BN][4] boxes
+  constexpr int STAGE = kKSub * BN * 4;  // doubles per stage: kKSub [BN][4] boxes
   static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile must be a multiple of 8x8");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -145,12 +148,13 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       int stage = 0;
       uint32_t phase = 0;
       for (int rt = rt_begin; rt < rt_end; ++rt) {
-        for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
+        for (int c = p.sub_begin / kKSub; c < p.nchunks; ++c) {
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], STAGE * sizeof(double));
           double* dst = Sst + size_t(stage) * STAGE;
-          tma_load_2d(dst, &tmap, &full[stage], c * 8, rt * BN, pol);
-          tma_load_2d(dst + BN * 4, &tmap, &full[stage], c * 8 + 4, rt * BN, pol);
+#pragma unroll
+          for (int j = 0; j < kKSub; ++j)
+            tma_load_2d(dst + j * BN * 4, &tmap, &full[stage], (c * kKSub + j) * 4, rt * BN, pol);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1u;
@@ -182,12 +186,12 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       for (int ni = 0; ni < NI; ++ni) accq[mi][ni][0] = accq[mi][ni][1] = 0.0;
 
     int q = 0, k0 = 0;  // current term and k offset of the sub-step (uniform over the warp)
-    for (int c = p.sub_begin / 2; c < p.nchunks; ++c) {
+    for (int c = p.sub_begin / kKSub; c < p.nchunks; ++c) {
       mbar_wait(&full[stage], phase);
       const double* st = Sst + size_t(stage) * STAGE;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int kap = 8 * c + 4 * j;
+      for (int j = 0; j < kKSub; ++j) {
+        const int kap = 4 * kKSub * c + 4 * j;
         if (kap >= 4 * p.nsub) break;
         if (kap < 4 * p.sub_begin) continue;
         double af[MI], bf[NI];
