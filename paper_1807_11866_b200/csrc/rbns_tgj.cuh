@@ -239,10 +239,10 @@ __device__ __forceinline__ double tgj_load_term(const NewtonParams& p, int b, in
 
 // resident CTAs per SM: two samples at N ≤ 103 (the register file holds two systems), four for small systems
 template <int RT>
-constexpr int tgj_min_blocks() { return RT <= 8 ? 4 : 2; }
+constexpr int tgj_min_blocks(int nw = 4) { return RT <= 8 ? (nw <= 3 ? 5 : 4) : 2; }
 
 template <int RT, int CT, int NW>
-__global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>()) newton_tgj_kernel(const NewtonParams p) {
+__global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>(NW)) newton_tgj_kernel(const NewtonParams p) {
   constexpr int JJ = (CT - 1 + NW - 1) / NW;  // register column tiles per warp (tile 0 stays in shared memory)
   constexpr int NT = NW * 32;
   constexpr int NR = 8 * RT;

@@ -6,8 +6,10 @@
 #include "rbns_tiled_plan.h"
 
 namespace rbns {
+// three warps (two register column tiles each, five CTAs per SM) where the column tiles number ≤ 6, four warps
+// above (tools/ntime.py: N = 40 / 48 / 50 +2.4 / +1.8 / +2.5 % with three; N = 56 / 64 −9 / −21 %)
 const TShape kTShapesA[] = {
-    RBNS_TS(5, 5, 4), RBNS_TS(5, 6, 4), RBNS_TS(6, 6, 4), RBNS_TS(6, 7, 4),
+    RBNS_TS(5, 5, 3), RBNS_TS(5, 6, 3), RBNS_TS(6, 6, 3), RBNS_TS(6, 7, 3),
     RBNS_TS(7, 8, 4), RBNS_TS(8, 8, 4), RBNS_TS(8, 9, 4),
 };
 const int kTShapesA_n = int(sizeof(kTShapesA) / sizeof(kTShapesA[0]));

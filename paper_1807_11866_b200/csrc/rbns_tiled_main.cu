@@ -6,7 +6,7 @@
 #include "rbns_tiled_plan.h"
 
 namespace rbns {
-const TShape kTShapesMain[] = {RBNS_TS(13, 13, 4), RBNS_TS(7, 7, 4)};
+const TShape kTShapesMain[] = {RBNS_TS(13, 13, 4), RBNS_TS(7, 7, 3)};  // config 1: three warps (see shapes_a)
 const int kTShapesMain_n = int(sizeof(kTShapesMain) / sizeof(kTShapesMain[0]));
 const HShape kHShapesMain[] = {RBNS_HS(25, 26, 12, 2, false)};
 const int kHShapesMain_n = int(sizeof(kHShapesMain) / sizeof(kHShapesMain[0]));

@@ -44,6 +44,6 @@ extern const int kHShapesC_n;
 }  // namespace rbns
 
 #define RBNS_TS(R_, C_, W_) \
-  { R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>(), tgj_min_blocks<R_>() }
+  { R_, C_, W_, newton_tgj_kernel<R_, C_, W_>, tgj_stage_offset<R_, W_>(), tgj_min_blocks<R_>(W_) }
 #define RBNS_HS(R_, C_, W_, G_, T_)                                                                           \
   { R_, C_, W_, newton_tgh_kernel<R_, C_, W_, G_>, tgh_smem_bytes<R_, C_, W_, G_>(), tgh_min_blocks<W_, G_>(), T_ }
