@@ -149,7 +149,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
       uint32_t phase = 0;
       for (int rt = rt_begin; rt < rt_end; ++rt) {
         for (int c = p.sub_begin / kKSub; c < p.nchunks; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1u);
+          // the producer lane sleeps between probes: spinning took issue slots from the consumer warps on its
+          // SM sub-partition (contraction 126.0 → 124.7 ms per cfg-2 step; 32–256 ns measured alike)
+          mbar_wait_backoff(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], STAGE * sizeof(double));
           double* dst = Sst + size_t(stage) * STAGE;
 #pragma unroll
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB)
 
     int q = 0, k0 = 0;  // current term and k offset of the sub-step (uniform over the warp)
     for (int c = p.sub_begin / kKSub; c < p.nchunks; ++c) {
-      mbar_wait(&full[stage], phase);
+      mbar_wait(&full[stage], phase);  // (a sleeping consumer wait measured slower: 126.0 vs 124.7 ms)
       const double* st = Sst + size_t(stage) * STAGE;
 #pragma unroll
       for (int j = 0; j < kKSub; ++j) {

@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(NW * 32, tgj_min_blocks<RT>(NW)) newton_tgj_ke
       const uint32_t par = (uint32_t(pc) / NB) & 1u;
       const int nx = P + 1;
       const bool own1 = nx < NP && warp == (nx - 1) % NW;
-      mbar_wait(&sh.full[s], par);
+      mbar_wait(&sh.full[s], par);  // (sleeping between probes here measured equal or slower)
       TGJ_TR(128 + 4 * P + warp);
       if (own1) {
         // critical path: panel P into tile nx, the inverse of its new pivot tile, publication of panel nx
