@@ -247,10 +247,18 @@ def run_ours(args, cfg, world, rank, local):
     from paper_1807_11866_b200 import online, synthetic
 
     dist = None
+    # RBNS_BENCH_BACKEND=gloo is a functional check of the N > 1 code path on a box with fewer GPUs than ranks
+    # (ranks share devices round-robin; their kernels never wait on one another): not a scaling measurement
+    backend = os.environ.get("RBNS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
 
@@ -432,6 +440,8 @@ def run_ours(args, cfg, world, rank, local):
                 "newton": {"sample_iterations_per_step": int(st["sample_iterations"]),
                            "converged": int((res.status == 0).sum().item()), "batch": batch}}
         line["bitwise_subset_check"] = subset_ok
+        if backend != "nccl":
+            line["functional_check"] = f"{backend} ranks sharing {torch.cuda.device_count()} device(s): not a scaling number"
         if compressed is not None:
             line["affine_compressed"] = compressed
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is timed at N = 1 only
