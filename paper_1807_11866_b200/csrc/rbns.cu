@@ -127,6 +127,13 @@ struct Operand {
   const rbns_theta_term* thl = nullptr;
   int stages = 0;
   size_t smem = 0;
+  oz::OperandI8 i8;                        // sliced copy for the tcgen05 INT8 path (A8 == NULL: DMMA only)
+};
+
+// per-call buffers of the INT8 path: the sliced X of one launch
+struct OzScratch {
+  uint8_t* B8 = nullptr;
+  double* sb = nullptr;
 };
 
 struct rbns_model {
@@ -162,8 +169,16 @@ constexpr ContractKernel kContract = contract_kernel<kBM, kBN, kWM, kWN>;
 
 int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n, const double* u, const double* mu,
                     double* out, int64_t ldo, cudaStream_t st, bool linear_only = false,
-                    const double* wts = nullptr, int64_t B = 0) {
+                    const double* wts = nullptr, int64_t B = 0, const OzScratch* ozs = nullptr, int* launches = nullptr) {
   if (n <= 0) return RBNS_OK;
+  if (launches) *launches = 1;
+  if (op.i8.A8 && wts && ozs && ozs->B8) {
+    // INT8-sliced path on the tcgen05 tensor cores (rbns_oz.cuh): X slicing + GEMM
+    RBNS_CUDA(oz::launch(op.i8, act, n, u, wts, m->N, m->Ne, op.Qb, op.Ql, linear_only, ozs->B8, ozs->sb, out, ldo,
+                         m->num_sms, st));
+    if (launches) *launches = linear_only ? 1 : 2;
+    return RBNS_OK;
+  }
   ContractParams p{};
   p.act = act;
   p.n = n;
@@ -388,6 +403,11 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
   RBNS_CUDA(ws.alloc(&miss_list, size_t(std::max<int64_t>(1, std::min<int64_t>(B, cap))) * sizeof(int32_t)));
   double* jbuf = nullptr;
   if (max_iter > 0) RBNS_CUDA(ws.alloc(&jbuf, size_t(cap) * ldj * sizeof(double)));
+  OzScratch ozs;
+  if (max_iter > 0 && m->vel.i8.A8) {
+    RBNS_CUDA(ws.alloc(&ozs.B8, oz::scratch_b8_bytes(m->vel.i8, cap)));
+    RBNS_CUDA(ws.alloc(&ozs.sb, oz::scratch_sb_bytes(cap)));
+  }
   static thread_local int32_t* hcount = nullptr;  // pinned, one per host thread for the process lifetime
   if (!hcount) RBNS_CUDA(cudaMallocHost(&hcount, 2 * sizeof(int32_t)));
 
@@ -438,11 +458,12 @@ int solve_device(rbns_model* m, const double* mu, int64_t B, double tol, int32_t
         // u = 0 at the first step: the convective part vanishes, only the affine block of the GEMM runs
         // (J = L(μ), h = 0); later steps run the full contraction
         const int e = timer.begin(first ? 3 : 0);
-        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first, wts, B);
+        int nl = 1;
+        rc = launch_contract(m, m->vel, act0 + c0, nc, u, mu, jbuf, ldj, st, first, wts, B, &ozs, &nl);
         timer.end(e);
         if (rc) break;
         stats.gemm_launches += 1;
-        stats.kernel_launches += 1;
+        stats.kernel_launches += nl;
       }
       const int e = timer.begin(1);
       int nl = 0;
@@ -764,6 +785,19 @@ int rbns_model_create2(const rbns_model_desc2* d, int device, rbns_model** out) 
   m->bytes = m->vel.rows * m->vel.kalloc * 8 + int64_t(m->Qf) * N * 8 + int64_t(th.size()) * 24;
   int rc = make_tensor_map(&m->vel.tm, m->vel.S, m->vel.rows, m->vel.kalloc);
   if (rc) return cleanup(rc);
+  {
+    // The velocity contraction runs on the tcgen05 INT8 tensor cores over error-free slices of S and X
+    // (rbns_oz.cuh) unless RBNS_CONTRACT=dmma asks for the FP64 DMMA kernel (read per model create).
+    const char* mode = std::getenv("RBNS_CONTRACT");
+    const bool want_i8 = !(mode && std::string(mode) == "dmma");
+    const int kterms = m->vel.Qb * m->Ne;
+    if (want_i8 && oz::supported(kterms, m->vel.Ql, max_smem)) {
+      if (!step(oz::prepare(), "oz::prepare") ||
+          !step(oz::build_operand(m->vel.S, m->vel.rows, kterms, m->vel.kalloc, m->vel.Ql, &m->vel.i8), "slice S"))
+        return bad();
+      m->bytes += oz::operand_bytes(m->vel.i8);
+    }
+  }
 
   if (m->Np) {
     const int64_t np = m->Np;
@@ -822,6 +856,7 @@ int rbns_model_destroy(rbns_model* m) {
                   static_cast<void*>(m->f), static_cast<void*>(m->L), static_cast<void*>(m->Lt),
                   static_cast<void*>(m->dth)})
     if (p) cudaFree(p);
+  oz::free_operand(&m->vel.i8);
   if (m->pool) cudaMemPoolDestroy(m->pool);  // every call has synchronized and freed its workspace
   delete m;
   return RBNS_OK;
