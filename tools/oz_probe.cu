@@ -165,7 +165,7 @@ int main(int argc, char** argv) {
                   tr[t * 8] - tr[0], tr[t * 8 + 1] - tr[t * 8], tr[t * 8 + 2] - tr[t * 8], tr[t * 8 + 3] - tr[t * 8],
                   tr[t * 8 + 4] - tr[t * 8]);
   }
-  for (int dbg = 1; dbg < 8 && reps > 0; ++dbg) {  // pipeline ablations (results are wrong by construction)
+  for (int dbg : {1, 2, 4, 8, 9}) {  // pipeline ablations (results are wrong by construction)
     GemmParams gd = gp;
     gd.dbg = dbg;
     oz_slice_X<<<sample_tiles * kTN / 8, 256>>>(sp);
@@ -174,7 +174,7 @@ int main(int argc, char** argv) {
     CK(cudaEventRecord(e1));
     CK(cudaDeviceSynchronize());
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    std::printf("ablation dbg=%d (1 no copies, 2 quarter MMAs, 4 no stores): gemm %.3f ms\n", dbg, ms);
+    std::printf("ablation dbg=%d (1 no copies, 2 first A slice only, 4 no stores, 8 drain only): gemm %.3f ms\n", dbg, ms);
   }
   for (int it = 0; it < reps; ++it) {
     CK(cudaEventRecord(e0));
