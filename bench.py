@@ -9,8 +9,9 @@ solves its own 65536-sample slice of one seeded μ stream); the only collectives
 the max-over-ranks reduction of the device time.
 
 The JSON line carries: value (whole-job solves/s, device-timed), e2e (same metric through the C-ABI host-buffer
-call rbns_solve_host with pinned host μ and results, copies inside the timed region), roofline (the DMMA
-contraction kernel against the FP64 peak measured live with cuBLAS DGEMM), cpu_baseline (the numpy oracle
+call rbns_solve_host with pinned host μ and results, copies inside the timed region), roofline (the contraction
+kernel: the INT8-sliced tcgen05 kernel against the INT8 tensor peak, with its FP64-equivalent rate beside the
+FP64 peak measured live with cuBLAS DGEMM; the DMMA alternate is timed as a secondary line), cpu_baseline (the numpy oracle
 on the host cores, bounded sample), clocks (nvidia-smi sampled during the timed region) and gpu_launches.
 
 ``--impl reference`` times the reference-side CPU implementation of the path (the oracle port in oracle/,
@@ -197,6 +198,36 @@ def fp64_peak(torch, device) -> dict:
     return {"tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "source": "live cuBLAS DGEMM 8192^3 burst (this run)"}
 
 
+def int8_peak(torch, device) -> dict:
+    """Dense INT8 tensor-core peak for the sliced contraction's roofline: cuBLASLt int8 GEMM 8192^3 measured in
+    this run (torch._int_mm, best of 5); else twice the bf16 figure of MEASURED_PEAKS.json (the INT8 rate of the
+    5th-generation tensor cores is twice the bf16 rate; the file has no INT8 entry); else the nominal 4.5 POP/s."""
+    n = 8192
+    try:
+        a = torch.randint(-8, 8, (n, n), dtype=torch.int8, device=device)
+        b = torch.randint(-8, 8, (n, n), dtype=torch.int8, device=device)
+        torch._int_mm(a, b)
+        torch.cuda.synchronize(device)
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize(device)
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return {"tops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "source": "live cuBLASLt INT8 GEMM 8192^3 burst (this run)"}
+    except Exception as exc:  # noqa: BLE001 - any failure falls through to the recorded figures
+        why = f"{type(exc).__name__}"
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return {"tops": 2.0 * float(mp["bf16_tflops"]),
+                "source": f"2 x MEASURED_PEAKS.json bf16_tflops (burst); live INT8 GEMM unavailable ({why})"}
+    except Exception:  # noqa: BLE001
+        return {"tops": 4500.0, "source": f"nominal dense INT8 4.5 POP/s (of fallback; live INT8 GEMM unavailable: {why})"}
+
+
 def traffic_from_profile(cfg_index: int):
     p = ROOT / "profiles" / "contract_traffic.json"
     if not p.exists():
@@ -343,6 +374,57 @@ def run_ours(args, cfg, world, rank, local):
         dmc.close()
         return mc, c_ms, c_gemm, rel, mism
 
+    # ---- secondary line: the same workload with the FP64 DMMA contraction (RBNS_CONTRACT=dmma, read at model
+    #      create) instead of the INT8-sliced tcgen05 contraction: the north-star's DMMA roofline figure ----
+    slices = dm.contraction_slices()
+
+    def measure_dmma():
+        if slices == 0:
+            return None
+        prev = os.environ.get("RBNS_CONTRACT")
+        os.environ["RBNS_CONTRACT"] = "dmma"
+        try:
+            dmd = online.DeviceModel(model, local)
+        finally:
+            if prev is None:
+                os.environ.pop("RBNS_CONTRACT", None)
+            else:
+                os.environ["RBNS_CONTRACT"] = prev
+        rd = None
+        for _ in range(args.warmup):
+            rd = dmd.solve(mu, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=rd)
+        d_ms, d_gemm, d_its = [], [], 0
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rd = dmd.solve(mu, tol=cfg.tol, max_iter=cfg.max_iter, pressure=pressure, out=rd)
+            e1.record(stream)
+            torch.cuda.synchronize(device)
+            d_ms.append(e0.elapsed_time(e1))
+            d_gemm.append(rd.stats["ms_gemm"])
+            d_its += rd.stats["contraction_iterations"]
+        rel = ((rd.u - res.u).abs().amax(dim=1) / res.u.abs().amax(dim=1)).max().item()
+        mism = int((rd.iters != res.iters).sum().item())
+        dmd.close()
+        return d_ms, d_gemm, d_its, rel, mism
+
+    dmma = None
+    try:
+        got_d = measure_dmma()
+    except Exception as exc:
+        print(f"bench: DMMA-contraction line skipped: {exc}", file=sys.stderr)
+        got_d = None
+    if got_d is not None:
+        d_ms, d_gemm, d_its, d_rel, d_mism = got_d
+        td = torch.tensor([float(np.mean(d_ms))], dtype=torch.float64, device=device)
+        if dist is not None:
+            dist.all_reduce(td, op=dist.ReduceOp.MAX)
+        dmma = {"value": batch * world / (float(td.item()) * 1e-3), "unit": UNIT, "ms_per_step": float(td.item()),
+                "ms_gemm_per_step": float(np.mean(d_gemm)),
+                "achieved_tflops": d_its * 2.0 * cfg.q * cfg.n ** 3 / (sum(d_gemm) * 1e-3) / 1e12,
+                "max_rel_diff_u_vs_main": d_rel, "iteration_count_mismatches": d_mism}
+
     compressed = None
     try:  # the secondary line must never cost the headline (a failure is systematic: every rank skips it)
         got = measure_compressed()
@@ -390,13 +472,42 @@ def run_ours(args, cfg, world, rank, local):
         peak = fp64_peak(torch, device)
         flops_per_launch = contraction_its / max(gemm_launches, 1) * 2.0 * cfg.q * cfg.n ** 3
         achieved = contraction_its * 2.0 * cfg.q * cfg.n ** 3 / (sum(gemm_ms) * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "contract_kernel (DMMA.8x8x4 + TMA)", "achieved": achieved,
-                "peak": peak["tflops"], "unit": "TFLOP/s", "frac": achieved / peak["tflops"],
-                "peak_source": peak["source"], "traffic": traffic_from_profile(cfg.index),
-                "algorithmic_flops_per_launch": flops_per_launch,
-                "flops_rule": "2*Q*N^3 per sample-iteration with u != 0 (SURVEY.md §8(d)); first Newton step "
-                              "has u = 0 and runs no contraction",
-                "gemm_share_of_step": float(np.sum(gemm_ms) / np.sum(step_ms))}
+        flops_rule = ("2*Q*N^3 per sample-iteration with u != 0 (SURVEY.md §8(d)); first Newton step has u = 0 and "
+                      "runs no contraction")
+        if slices == 0:
+            roof = {"bound": "tensor", "kernel": "contract_kernel (DMMA.8x8x4 + TMA)", "achieved": achieved,
+                    "peak": peak["tflops"], "unit": "TFLOP/s", "frac": achieved / peak["tflops"],
+                    "peak_source": peak["source"], "traffic": traffic_from_profile(cfg.index),
+                    "algorithmic_flops_per_launch": flops_per_launch, "flops_rule": flops_rule,
+                    "gemm_share_of_step": float(np.sum(gemm_ms) / np.sum(step_ms))}
+        else:
+            # The contraction runs as exact INT8 MMAs over `slices` digits per operand entry: every FP64
+            # multiply-add of the 2*Q*N^3 rule costs slices*(slices+1)/2 INT8 multiply-adds (the slice pairs
+            # i + j < slices) on the rows r < N^2 + G*N of the operand.
+            pairs = slices * (slices + 1) // 2
+            rows = cfg.n * cfg.n + cfg.n  # J rows + one residual-helper group (the BASELINE configs)
+            ops_per_it = 2.0 * pairs * rows * cfg.q * cfg.n
+            ipeak = int8_peak(torch, device)
+            tops = contraction_its * ops_per_it / (sum(gemm_ms) * 1e-3) / 1e12
+            roof = {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, TMEM accumulators, "
+                    f"cp.async.bulk operand images; {slices} slices, {pairs} slice products) + oz_slice_X",
+                    "achieved": tops, "peak": ipeak["tops"], "unit": "TOP/s", "frac": tops / ipeak["tops"],
+                    "peak_source": ipeak["source"], "traffic": traffic_from_profile(cfg.index),
+                    "algorithmic_ops_per_launch": contraction_its / max(gemm_launches, 1) * ops_per_it,
+                    "ops_rule": f"2 * {pairs} slice products * (N^2 + N) rows * Q*N columns per sample-iteration "
+                                "with u != 0; timed with the X slicing kernel of each launch",
+                    "fp64_equivalent": {"achieved": achieved, "unit": "TFLOP/s", "dgemm_peak": peak["tflops"],
+                                        "ratio_to_dgemm_peak": achieved / peak["tflops"],
+                                        "peak_source": peak["source"], "flops_rule": flops_rule},
+                    "gemm_share_of_step": float(np.sum(gemm_ms) / np.sum(step_ms))}
+            if dmma is not None:
+                dmma["roofline"] = {"bound": "tensor", "kernel": "contract_kernel (DMMA.8x8x4 + TMA)",
+                                    "achieved": dmma.pop("achieved_tflops"), "peak": peak["tflops"], "unit": "TFLOP/s",
+                                    "peak_source": peak["source"]}
+                dmma["roofline"]["frac"] = dmma["roofline"]["achieved"] / peak["tflops"]
+                dmma["note"] = ("the same workload with RBNS_CONTRACT=dmma: the FP64 tensor-core (DMMA) contraction "
+                                "the north star names, kept as the alternate path; the headline runs the INT8-sliced "
+                                "tcgen05 contraction (same sums to binary64 round-off, identical Newton counts)")
         # whole-step FP64 roofline with the full per-iteration flop count: contraction
         # 2QN³ (u ≠ 0 only), linear assembly 2QN², loads 2QN, LU (2/3)N³, residual + solves 6N²
         n3, n2 = cfg.n ** 3, cfg.n ** 2
@@ -444,6 +555,8 @@ def run_ours(args, cfg, world, rank, local):
             line["functional_check"] = f"{backend} ranks sharing {torch.cuda.device_count()} device(s): not a scaling number"
         if compressed is not None:
             line["affine_compressed"] = compressed
+        if dmma is not None:
+            line["contraction_dmma"] = dmma
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is timed at N = 1 only
             line["cpu_baseline"] = cpu_baseline(cfg, model, mu_np, min(args.cpu_sample or work_scaled(cfg, 65536), batch))
         print(json.dumps(line), flush=True)

@@ -165,6 +165,10 @@ int rbns_model_destroy(rbns_model* model);
 int rbns_model_info(const rbns_model* model, int32_t* n, int32_t* q, int32_t* n_p, int32_t* device);
 /* bytes of device memory the handle owns */
 int64_t rbns_model_device_bytes(const rbns_model* model);
+/* Contraction path of the handle's velocity operand: 0 = FP64 DMMA kernel (rbns_contract.cuh); s > 0 = the
+ * tcgen05 INT8 kernel over s error-free slices per operand entry (rbns_oz.cuh; the default, RBNS_CONTRACT=dmma
+ * at model create selects the DMMA kernel).  Both evaluate the same sums to binary64 round-off. */
+int rbns_model_contraction_slices(const rbns_model* model);
 
 /* Batched velocity-only Newton solve + optional pressure recovery, device buffers.
  *   mu          dev  B x 2   (alpha [rad], Re)

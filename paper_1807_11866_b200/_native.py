@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "CONVERGED", 1: "NON_CONVERGED", 2: "SINGULAR_SYSTEM", 3: "SI
 # every symbol include/rbns.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (
     "rbns_model_create", "rbns_model_create2", "rbns_model_terms", "rbns_model_destroy", "rbns_model_info",
-    "rbns_model_device_bytes", "rbns_model_attached", "rbns_solve", "rbns_solve_ex", "rbns_solve_host",
+    "rbns_model_device_bytes", "rbns_model_contraction_slices", "rbns_model_attached", "rbns_solve", "rbns_solve_ex", "rbns_solve_host",
     "rbns_solve_host_ex", "rbns_reduced_operator", "rbns_recover_pressure", "rbns_reconstruct_pressure",
     "rbns_get_stats", "rbns_project_convection", "rbns_error_string", "rbns_last_error_message",
     "rbns_abi_version",
@@ -92,6 +92,8 @@ def load(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.rbns_model_info.argtypes = [vp] + [ctypes.POINTER(i32)] * 4
     lib.rbns_model_device_bytes.argtypes = [vp]
     lib.rbns_model_device_bytes.restype = i64
+    lib.rbns_model_contraction_slices.argtypes = [vp]
+    lib.rbns_model_contraction_slices.restype = ctypes.c_int
     solve_args = [vp, vp, i64, dbl, i32, vp, vp, vp, vp, vp, vp]
     lib.rbns_solve.argtypes = solve_args
     lib.rbns_solve_host.argtypes = solve_args

@@ -884,6 +884,8 @@ int rbns_model_terms(const rbns_model* m, int32_t counts[6]) {
 
 int64_t rbns_model_device_bytes(const rbns_model* m) { return m ? m->bytes : 0; }
 
+int rbns_model_contraction_slices(const rbns_model* m) { return (m && m->vel.i8.A8) ? oz::slices() : 0; }
+
 int rbns_get_stats(const rbns_model* m, rbns_stats* out) {
   if (!m || !out) return fail(RBNS_ERR_INVALID_ARGUMENT, "NULL argument");
   std::lock_guard<std::mutex> lk(const_cast<rbns_model*>(m)->stats_mu);

@@ -29,6 +29,7 @@ struct OperandI8 {
   int k32 = 0, kchunks = 0, Ql = 0;
   int64_t row_tiles = 0;
 };
+int slices();                              // digits per operand entry (compile-time RBNS_OZ_SLICES)
 cudaError_t prepare();                     // function attributes, call with the model's device current
 bool supported(int K, int Ql, int max_smem);  // K = θ ⊗ u columns, Ql = affine columns
 // slices the leading K columns of S (rows × ldS) and gathers the Ql affine columns that follow them

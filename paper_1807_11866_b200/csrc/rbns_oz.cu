@@ -9,6 +9,8 @@
 namespace rbns {
 namespace oz {
 
+int slices() { return kS; }
+
 cudaError_t prepare() {
   return cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes));
 }

@@ -161,6 +161,10 @@ class DeviceModel:
     def device_bytes(self) -> int:
         return int(self.lib.rbns_model_device_bytes(self._h))
 
+    def contraction_slices(self) -> int:
+        """0: the FP64 DMMA contraction; s > 0: the tcgen05 INT8 contraction over s slices per entry (default)."""
+        return int(self.lib.rbns_model_contraction_slices(self._h))
+
     def stats(self) -> dict:
         """Statistics of the most recent solve on this handle (per-call numbers are in BatchSolution.stats)."""
         st = _native.StatsC()

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU session: bench line (+ reference arm), plain run + ncu launch list of one bench step, full ncu capture
-# of the two hot kernels (contraction + tiled Newton update) on a fixed cfg-2 workload, and of the cfg-3 Newton
+# of the two hot kernels (INT8-sliced contraction + tiled Newton update) on a fixed cfg-2 workload, and of the cfg-3 Newton
 # kernel on a 4096-sample cfg-3 workload.
 set -x
 mkdir -p gpurun_out
@@ -12,7 +12,7 @@ $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 P="python tools/profile_case.py 2 65536"
 $P > gpurun_out/plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"contract_kernel" -s 2 -c 1 -o gpurun_out/full $P > gpurun_out/ncu_full.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"oz_gemm_kernel" -s 2 -c 1 -o gpurun_out/full $P > gpurun_out/ncu_full.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"newton_tgj" -s 2 -c 1 -o gpurun_out/full_lu $P > gpurun_out/ncu_full_lu.log 2>&1
 P3="python tools/profile_case.py 3 4096"
 $P3 > gpurun_out/plain3.log 2>&1 && \
