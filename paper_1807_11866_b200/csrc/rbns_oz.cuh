@@ -299,9 +299,22 @@ __host__ __device__ constexpr uint32_t idesc_n(int n) {
 constexpr int kWide = RBNS_OZ_WIDE;  // X slices per MMA (N = 64·kWide ≤ 256)
 static_assert(kWide >= 1 && kWide * kTN <= 256, "MMA N");
 
-__device__ __forceinline__ double i32_to_f64(int x) {
+__host__ __device__ __forceinline__ double i32_to_f64(int x) {
+#ifdef __CUDA_ARCH__
   // 2^52 + 2^31 + x as a bit pattern, minus the constant: exact, no I2F
   return __hiloint2double(0x43300000, x ^ int(0x80000000)) - 4503601774854144.0;
+#else
+  return double(x);
+#endif
+}
+
+// Σ_g a_g·2^{−8g} for one output from its kS group sums: Horner in binary64, smallest group first.  (Measured and
+// not kept: adjacent groups combined exactly in int64, one conversion per pair — the same drain time.)
+__host__ __device__ __forceinline__ double combine_groups(const int (&a)[kS]) {
+  double t = i32_to_f64(a[kS - 1]);
+#pragma unroll
+  for (int g = kS - 2; g >= 0; --g) t = fma(t, 0.00390625, i32_to_f64(a[g]));
+  return t;
 }
 
 struct GemmParams {
@@ -481,10 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
         double y[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          double t = i32_to_f64(v[kS - 1][e]);
+          int a[kS];
 #pragma unroll
-          for (int g = kS - 2; g >= 0; --g) t = fma(t, 0.00390625, i32_to_f64(v[g][e]));
-          y[e] = t * sar * sbS[c0 + e];
+          for (int g = 0; g < kS; ++g) a[g] = v[g][e];
+          y[e] = combine_groups(a) * sar * sbS[c0 + e];
         }
 #pragma unroll
         for (int a = 0; a < kMaxAff; ++a) {

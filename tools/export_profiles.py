@@ -37,7 +37,7 @@ def launch_summary(path):
     lines.append(f"{'total':60s} {sum(v[0] for v in agg.values()):8d} {tot:10.3f}")
     # the solver's own kernels only (the step): the cutlass DGEMMs are bench.py's in-run FP64 peak measurement,
     # the at:: kernels its input generation and L2 flush
-    own = {k: v for k, v in agg.items() if k.startswith("rbns::")}
+    own = {k: v for k, v in agg.items() if k.startswith(("rbns::", "oz::"))}
     tot_own = sum(v[1] for v in own.values())
     lines += ["", "solver kernels only (shares of the solve; bench.py's cutlass DGEMMs measure the FP64 peak):",
               f"{'kernel':60s} {'launches':>8s} {'ms':>10s} {'share':>6s}"]
@@ -66,7 +66,8 @@ def main():
         rows = list(csv.reader(io.StringIO(raw)))
         hdr = rows[0]
         for r in rows[2:]:
-            if "contract_kernel" not in r[hdr.index("Kernel Name")]:
+            kname = r[hdr.index("Kernel Name")]
+            if "contract_kernel" not in kname and "oz_gemm_kernel" not in kname:
                 continue
             rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
             wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
@@ -79,7 +80,10 @@ def main():
                 "dram_write_bytes": int(wr * scale),
                 "launch": f"{r[hdr.index('Kernel Name')]} grid {r[hdr.index('Grid Size')]} = full 65536-sample Newton round",
                 "source": f"profiles/{tag}_ncu_full_raw.csv (ncu --set full, cold cache; .ncu-rep kept out of git)",
-                "note": "reads = S (56 MB, L2-resident) + u tiles; writes = the Jacobians J (65536 x 10112 x 8 B)"}},
+                "note": ("reads = the sliced X images (8 x 65536 x 704 B, re-read per row tile through L2) + the "
+                         "sliced S (52 MB, L2-resident); writes = the Jacobians J (65536 x 10112 x 8 B)")
+                if "oz_gemm" in kname else
+                "reads = S (56 MB, L2-resident) + u tiles; writes = the Jacobians J (65536 x 10112 x 8 B)"}},
                 open(PROF / "contract_traffic.json", "w"), indent=1)
             break
     print(sorted(p.name for p in PROF.iterdir() if p.name.startswith(tag)))

@@ -242,9 +242,9 @@ int main(int argc, char** argv) {
       for (int k = 0; k < k32; ++k)
         for (int i = 0; i < kS; ++i)
           for (int j = 0; j < kS - i; ++j) acc[i + j] += (long long)sd[k * kS + i] * xd[bi][k * kS + j];
-      double t = double(acc[kS - 1]);
-      for (int g = kS - 2; g >= 0; --g) t = std::fma(t, 0.00390625, double(acc[g]));
-      double emu = t * ss * xs[bi];
+      int a32[kS];
+      for (int g = 0; g < kS; ++g) a32[g] = int(acc[g]);
+      double emu = combine_groups(a32) * ss * xs[bi];
       for (int a = 0; a < Ql; ++a) emu = std::fma(xv[bi][kterms + a], S[size_t(r) * K + kterms + a], emu);
       const double got = out[size_t(bsel[bi]) * ldo + r];
       if (!(emu == got)) {
