@@ -76,6 +76,24 @@ def build_checked(force: bool = False) -> Path:
     return build(force=force, out=CHECKED, extra=("-DRBNS_CHECKED",))
 
 
+PROBE = ROOT / "build" / "oz_probe"
+
+
+def build_probe(force: bool = False) -> Path:
+    """tools/oz_probe.cu: the INT8-sliced contraction kernel against a host emulation of the same splitting, bit
+    for bit (tests/test_oz.py runs it on the GPU)."""
+    src = ROOT / "tools" / "oz_probe.cu"
+    deps = [src, CSRC / "rbns_oz.cuh", CSRC / "rbns_common.cuh", ROOT / "include" / "rbns.h"]
+    if PROBE.exists() and not force and all(PROBE.stat().st_mtime >= d.stat().st_mtime for d in deps):
+        return PROBE
+    PROBE.parent.mkdir(parents=True, exist_ok=True)
+    r = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+                        f"-I{ROOT / 'include'}", f"-I{CSRC}", str(src), "-o", str(PROBE)], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
+    return PROBE
+
+
 if __name__ == "__main__":
     if "--define" in sys.argv:  # development variant: python -m ...build --define NAME=VAL  -> build/librbns_NAME.so
         d = sys.argv[sys.argv.index("--define") + 1]

@@ -175,7 +175,7 @@ int launch_contract(rbns_model* m, const Operand& op, const int32_t* act, int n,
   if (op.i8.A8 && wts && ozs && ozs->B8) {
     // INT8-sliced path on the tcgen05 tensor cores (rbns_oz.cuh): X slicing + GEMM
     RBNS_CUDA(oz::launch(op.i8, act, n, u, wts, m->N, m->Ne, op.Qb, op.Ql, linear_only, ozs->B8, ozs->sb, out, ldo,
-                         m->num_sms, st));
+                         m->num_sms, st, B));
     if (launches) *launches = linear_only ? 1 : 2;
     return RBNS_OK;
   }
@@ -1020,6 +1020,13 @@ extern "C" int rbns_debug_checks(int* line_main, int* line_newton, unsigned long
   int ln = 0;
   unsigned long long cn = 0;
   if (rbns::newton_debug_checks(&ln, &cn)) return 2;
+  {
+    int lo = 0;  // the INT8 contraction's translation unit: folded into the main line / total count
+    unsigned long long co = 0;
+    if (rbns::oz::debug_checks(&lo, &co)) return 2;
+    if (ln == 0) ln = lo;
+    cn += co;
+  }
 #ifdef RBNS_CHECKED
   int lm = 0;
   unsigned long long cm = 0;

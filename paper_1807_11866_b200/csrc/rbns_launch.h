@@ -41,7 +41,9 @@ size_t scratch_sb_bytes(int64_t cap);
 // Y[i][r] = Σ_κ X[i][κ] S[r][κ] for the n samples act[0..n) (NULL = identity): slices X, runs the GEMM
 cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double* u, const double* wts, int N, int Ne,
                    int Qb, int Ql, bool zero_u, uint8_t* B8, double* sb, double* out, int64_t ldo, int num_sms,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t B = 0);
+// checked builds: this translation unit's failed-check counters
+int debug_checks(int* line, unsigned long long* count);
 }  // namespace oz
 
 // checked builds (-DRBNS_CHECKED): this translation unit's failed-check counters (first source line, count)

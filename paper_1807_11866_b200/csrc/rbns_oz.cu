@@ -61,7 +61,7 @@ size_t scratch_sb_bytes(int64_t cap) { return size_t((cap + kTN - 1) / kTN) * kT
 
 cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double* u, const double* wts, int N, int Ne,
                    int Qb, int Ql, bool zero_u, uint8_t* B8, double* sb, double* out, int64_t ldo, int num_sms,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t B) {
   if (n <= 0) return cudaSuccess;
   const int sample_tiles = (n + kTN - 1) / kTN;
   if (!zero_u) {
@@ -78,6 +78,7 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
     sp.k32 = op.k32;
     sp.B8 = B8;
     sp.sb = sb;
+    sp.B = B;
     oz_slice_X<<<sample_tiles * kTN / 8, 256, 0, st>>>(sp);
   }
   GemmParams gp{};
@@ -99,6 +100,7 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
   gp.Qb = Qb;
   gp.Ql = Ql;
   gp.ldw = Qb + Ql;
+  gp.B = B;
   // CTAs per launch: every sample tile, split over row-tile groups until the grid covers a few waves
   const int64_t want = int64_t(4) * num_sms;
   int groups = int(std::max<int64_t>(1, (want + sample_tiles - 1) / sample_tiles));
@@ -107,6 +109,18 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
   groups = int((op.row_tiles + gp.tiles_per_group - 1) / gp.tiles_per_group);
   oz_gemm_kernel<<<dim3(sample_tiles, groups), kThreads, kSmemBytes, st>>>(gp);
   return cudaGetLastError();
+}
+
+int debug_checks(int* line, unsigned long long* count) {
+#ifdef RBNS_CHECKED
+  if (cudaMemcpyFromSymbol(line, rbns::g_chk_line, sizeof(int)) != cudaSuccess ||
+      cudaMemcpyFromSymbol(count, rbns::g_chk_count, sizeof(unsigned long long)) != cudaSuccess)
+    return 2;
+#else
+  *line = 0;
+  *count = 0;
+#endif
+  return 0;
 }
 
 }  // namespace oz

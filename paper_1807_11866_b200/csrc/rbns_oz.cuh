@@ -207,6 +207,7 @@ struct SliceXParams {
   int32_t N, Ne, Qb, Ql, k32;  // κ = j·Ne + k over the Qb blocks (the Ql affine weights follow the block weights in wts)
   uint8_t* B8;          // [sample_tiles][kc][slice][image(64)]
   double* sb;           // [sample_tiles·64]
+  int64_t B;            // samples of the call (sample ids < B; checked builds), 0 = n
 };
 
 __global__ void oz_slice_X(const SliceXParams p) {
@@ -214,6 +215,8 @@ __global__ void oz_slice_X(const SliceXParams p) {
   const int lane = threadIdx.x & 31;
   const bool live = i < p.n;
   const int id = live ? (p.act ? p.act[i] : i) : 0;
+  RBNS_CHECK(id >= 0 && id < (p.B > 0 ? p.B : p.n));
+  RBNS_CHECK(i < ((p.n + kTN - 1) / kTN) * kTN);
   const double* u = p.u + int64_t(id) * p.N;
   const double* w = p.wts + int64_t(id) * (p.Qb + p.Ql);
   const int kterms = p.Qb * p.Ne;
@@ -333,6 +336,7 @@ struct GemmParams {
   const int32_t* act; // sample ids (NULL = identity)
   int32_t Qb, Ql, ldw;
   int32_t no_acc;     // u = 0 launch: no MMAs, the affine part only
+  int64_t B;          // samples of the call (sample ids < B; checked builds), 0 = n
   long long* trace;   // probe only: clock64 stamps of CTA (0,0)
   int32_t dbg;        // probe only: 1 = no copies after the ring is primed, 2 = first A slice only, 4 = no stores, 8 = drain only
 };
@@ -368,10 +372,12 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
     const int i = st * kTN + c;
     double v = 0.0;
     if (i < p.n) {
+      const int id = p.act ? p.act[i] : i;
+      RBNS_CHECK(id >= 0 && id < (p.B > 0 ? p.B : p.n));
       if (a < 0)
         v = p.no_acc ? 0.0 : p.sb[i];
       else
-        v = p.wts[int64_t(p.act ? p.act[i] : i) * p.ldw + p.Qb + a];
+        v = p.wts[int64_t(id) * p.ldw + p.Qb + a];
     }
     if (a < 0)
       sbS[c] = v;
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       int stage = 0;
       uint32_t phase = 0;
       for (int rt = rt_begin; rt < rt_end; ++rt) {
+        RBNS_CHECK(rt >= 0 && rt < p.row_tiles && p.kc_begin >= 0 && p.kc_begin <= p.kchunks);
         const uint8_t* a = p.A8 + (size_t(rt) * p.kchunks + p.kc_begin) * kAStage;
         const uint8_t* b = p.B8 + (size_t(st) * p.kchunks + p.kc_begin) * kBStage;
         for (int kc = p.kc_begin; kc < p.kchunks; ++kc, a += kAStage, b += kBStage) {
@@ -466,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
     uint32_t tphase = 0;
     for (int rt = rt_begin; rt < rt_end; ++rt) {
       const int64_t r = int64_t(rt) * kTM + q * 32 + lane;
+      RBNS_CHECK(r < p.ldo && r < p.aff_ld);
       // this row's scale and affine entries, fetched while the MMAs of the tile run
       const double sar = p.no_acc ? 0.0 : p.sa[r];
       double aff[kMaxAff];

@@ -99,13 +99,9 @@ def test_sliced_dot_products_reach_binary64_accuracy():
 def test_probe_kernel_is_bit_exact(tmp_path):
     """tools/oz_probe.cu: the tcgen05 kernel's output equals the host emulation of the same splitting for every
     checked (sample, row) pair, on a shape with partial tiles (N = 37: 1406 rows, 300 samples)."""
-    exe = ROOT / "build" / "oz_probe"
-    src = ROOT / "tools" / "oz_probe.cu"
-    hdr = ROOT / "paper_1807_11866_b200" / "csrc" / "rbns_oz.cuh"
-    if not exe.exists() or exe.stat().st_mtime < max(src.stat().st_mtime, hdr.stat().st_mtime):
-        exe.parent.mkdir(exist_ok=True)
-        subprocess.run(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-                        f"-I{ROOT / 'include'}", f"-I{hdr.parent}", str(src), "-o", str(exe)], check=True)
+    from paper_1807_11866_b200 import build
+
+    exe = build.build_probe()
     for args in (["300", "37", "3", "1"], ["4096", "100", "7", "1"]):
         r = subprocess.run([str(exe), *args], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and "0 mismatches vs host emulation" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
