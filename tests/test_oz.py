@@ -12,22 +12,21 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 KS = 8                                              # RBNS_OZ_SLICES
-TAU = float.fromhex("0x1.fdfdfdfdfdfdfp-2")         # largest binary64 below 127/255 (rbns_oz.cuh kTau)
+BAL = 0x0080808080808080                            # 0x80 in every byte below the top one (rbns_oz.cuh kBal)
 
 
 def digits(v, ks=KS):
-    """numpy restatement of rbns::oz::digits: balanced radix-256 digits of v in (-1/2, 1/2)."""
-    r = np.asarray(v, dtype=np.float64) * 0.5
-    out = []
-    for _ in range(ks):
-        w = r * 256.0
-        q = np.maximum(np.rint(w), -128.0)
-        r = w - q
-        up = r > TAU
-        q = np.where(up, q + 1.0, q)
-        r = np.where(up, r - 1.0, r)
-        out.append(q)
-    return np.array(out), r
+    """numpy restatement of rbns::oz::digits: F = rint(v·2^(8s-1)), balanced radix-256 digits = bytes of
+    (F + C) xor C; returns the digits (most significant first) and the rounding remainder in units of 2^-(8s-1)."""
+    assert ks == 8
+    v = np.asarray(v, dtype=np.float64)
+    f = v * 2.0 ** 63
+    F = np.rint(f)
+    rem = f - F
+    t = (F.astype(np.int64).astype(np.uint64) + np.uint64(BAL)) ^ np.uint64(BAL)
+    out = [((t >> np.uint64(8 * (ks - 1 - i))) & np.uint64(0xFF)).astype(np.uint8).view(np.int8).astype(np.float64)
+           for i in range(ks)]
+    return np.array(out), rem
 
 
 def slice_row(v, ks=KS):
@@ -45,17 +44,17 @@ def test_digits_are_bytes_and_exact():
     v = rng.uniform(-0.5, 0.5, 400_000)
     v[::3] *= 1e-6
     v[::7] *= 1e-12
-    edge = np.array([0.0, 0.5 - 2.0 ** -54, -0.5 + 2.0 ** -54, 127.0 / 255.0 / 128.0, TAU / 128.0, 2.0 ** -60,
+    edge = np.array([0.0, 0.5 - 2.0 ** -54, -0.5 + 2.0 ** -54, 127.0 / 255.0 / 128.0, 2.0 ** -64, 2.0 ** -60,
                      -(2.0 ** -60), 0.25, -0.25, 1.0 / 3.0, -1.0 / 3.0])
     v = np.concatenate([v, edge])
     d, r = digits(v)
-    assert d[0].min() >= -64 and d[0].max() <= 65
+    assert d[0].min() >= -64 and d[0].max() <= 64
     assert d.min() >= -128 and d.max() <= 127
-    assert np.all(r >= -128.0 / 255.0 - 1e-15) and np.all(r <= 127.0 / 255.0)
-    # exact reconstruction: v = Σ d_i 2^{-7-8i} + r·2^{-7-8(s-1)} in rational arithmetic
+    assert np.all(np.abs(r) <= 0.5)
+    # exact reconstruction: v = Σ d_i 2^{-7-8i} + r·2^{-(8s-1)} in rational arithmetic
     for k in list(range(0, len(v), 9973)) + list(range(len(v) - len(edge), len(v))):
         acc = sum(Fraction(int(d[i][k])) / Fraction(2) ** (7 + 8 * i) for i in range(KS))
-        acc += Fraction(float(r[k])) / Fraction(2) ** (7 + 8 * (KS - 1))
+        acc += Fraction(float(r[k])) / Fraction(2) ** (8 * KS - 1)
         assert acc == Fraction(float(v[k])), k
     # truncation bound of the kept digits
     w = 2.0 ** -(7.0 + 8.0 * np.arange(KS))
