@@ -491,7 +491,8 @@ def run_ours(args, cfg, world, rank, local):
             tops = contraction_its * ops_per_it / (sum(gemm_ms) * 1e-3) / 1e12
             roof = {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, TMEM accumulators, "
                     f"cp.async.bulk operand images; {slices} slices, {pairs} slice products) + oz_slice_X",
-                    "achieved": tops, "peak": ipeak["tops"], "unit": "TOP/s", "frac": tops / ipeak["tops"],
+                    "achieved": tops, "peak": ipeak["tops"], "unit": "TFLOP/s", "frac": tops / ipeak["tops"],
+                    "op_type": "INT8 tensor operations (one multiply-add = 2 ops), i.e. TOP/s, for achieved and peak",
                     "peak_source": ipeak["source"], "traffic": traffic_from_profile(cfg.index),
                     "algorithmic_ops_per_launch": contraction_its / max(gemm_launches, 1) * ops_per_it,
                     "ops_rule": f"2 * {pairs} slice products * (N^2 + N) rows * Q*N columns per sample-iteration "

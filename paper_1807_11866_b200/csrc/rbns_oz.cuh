@@ -347,6 +347,21 @@ __host__ __device__ __forceinline__ double combine_groups(const int (&a)[kS]) {
   return t;
 }
 
+// Pipeline ablations and clock64 stamps exist only in the probe build (tools/oz_probe.cu defines RBNS_OZ_PROBE);
+// in the library the conditions are compile-time false.
+#ifdef RBNS_OZ_PROBE
+#define OZ_DBG(p, bit) (((p).dbg & (bit)) != 0)
+#define OZ_STAMP(p, cond, slot) \
+  do {                          \
+    if ((p).trace && (cond)) (p).trace[slot] = clock64(); \
+  } while (0)
+#else
+#define OZ_DBG(p, bit) false
+#define OZ_STAMP(p, cond, slot) \
+  do {                          \
+  } while (0)
+#endif
+
 struct GemmParams {
   const uint8_t* A8;  // [row_tiles][kchunks][kS][kAImg]
   const uint8_t* B8;  // [sample_tiles][kchunks][kS][kBImg]
@@ -364,8 +379,10 @@ struct GemmParams {
   int32_t Qb, Ql, ldw;
   int32_t no_acc;     // u = 0 launch: no MMAs, the affine part only
   int64_t B;          // samples of the call (sample ids < B; checked builds), 0 = n
-  long long* trace;   // probe only: clock64 stamps of CTA (0,0)
-  int32_t dbg;        // probe only: 1 = no copies after the ring is primed, 2 = first A slice only, 4 = no stores, 8 = drain only
+#ifdef RBNS_OZ_PROBE
+  long long* trace;   // clock64 stamps of CTA (0,0)
+  int32_t dbg;        // 1 = no copies after the ring is primed, 2 = first A slice only, 4 = no stores, 8 = drain only
+#endif
 };
 
 __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p) {
@@ -428,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
         const uint8_t* b = p.B8 + (size_t(st) * p.kchunks + p.kc_begin) * kBStage;
         for (int kc = p.kc_begin; kc < p.kchunks; ++kc, a += kAStage, b += kBStage) {
           mbar_wait_backoff(&empty[stage], phase ^ 1u);
-          if ((p.dbg & 1) && (rt > rt_begin || kc >= p.kc_begin + kStages)) {
+          if (OZ_DBG(p, 1) && (rt > rt_begin || kc >= p.kc_begin + kStages)) {
             mbar_arrive(&full[stage]);
           } else {
             mbar_arrive_expect_tx(&full[stage], kStageBytes);
@@ -456,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       mbar_wait(tempty, tphase ^ 1u);  // epilogue drained the previous tile's accumulators
       tphase ^= 1u;
       tc_fence_after();
-      if (p.trace && leader && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4) p.trace[(rt - rt_begin) * 8 + 0] = clock64();
+      OZ_STAMP(p, leader && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4, (rt - rt_begin) * 8 + 0);
       for (int kc = p.kc_begin; kc < p.kchunks; ++kc) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -471,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
           // stage is bound by the MMA rate, not by shared-memory reads (12 MMAs per stage instead of 36).
 #pragma unroll
           for (int i = 0; i < kS; ++i) {
-            if ((p.dbg & 2) && i > 0) break;
+            if (OZ_DBG(p, 2) && i > 0) break;
             const uint64_t ad = make_desc(alo + uint32_t(i) * (kAImg >> 4), kDescHi);
 #pragma unroll
             for (int j = 0; j < kS - i; j += kWide) {
@@ -490,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       }
       if (leader) mma_commit(tfull);  // accumulators of this tile complete (at once on the u = 0 launch: no MMAs)
       __syncwarp();
-      if (p.trace && leader && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4) p.trace[(rt - rt_begin) * 8 + 1] = clock64();
+      OZ_STAMP(p, leader && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4, (rt - rt_begin) * 8 + 1);
     }
   } else {
     // ---------------- epilogue: TMEM -> binary64 (+ affine columns) -> J buffer ----------------
@@ -509,8 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       mbar_wait(tfull, tphase);
       tphase ^= 1u;
       tc_fence_after();
-      const bool tr = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4 && warp == 2 && lane == 0;
-      if (tr) p.trace[(rt - rt_begin) * 8 + 2] = clock64();
+      [[maybe_unused]] const bool tr = blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4 && warp == 2 && lane == 0;
+      OZ_STAMP(p, tr, (rt - rt_begin) * 8 + 2);
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 8) {
         int v[kS][8];
@@ -520,9 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
         if (c0 + 8 == cbeg + kCols) {
           tc_fence_before();
           mbar_arrive(tempty);
-          if (tr) p.trace[(rt - rt_begin) * 8 + 3] = clock64();
+          OZ_STAMP(p, tr, (rt - rt_begin) * 8 + 3);
         }
-        if (p.dbg & 8) {  // probe: drain only
+        if (OZ_DBG(p, 8)) {  // probe: drain only
           if (v[0][0] == 0x7fffffff) p.out[0] = 0.0;
           continue;
         }
@@ -542,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
             for (int e = 0; e < 8; ++e) y[e] = fma(wa[e], aff[a], y[e]);
           }
         }
-        if (!(p.dbg & 4)) {
+        if (!OZ_DBG(p, 4)) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int i = st * kTN + c0 + e;
@@ -550,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
           }
         }
       }
-      if (tr) p.trace[(rt - rt_begin) * 8 + 4] = clock64();
+      OZ_STAMP(p, tr, (rt - rt_begin) * 8 + 4);
     }
   }
   tc_fence_before();

@@ -11,6 +11,7 @@
 #include <random>
 #include <vector>
 
+#define RBNS_OZ_PROBE 1
 #include "rbns_oz.cuh"
 
 using namespace rbns;
