@@ -64,7 +64,23 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
                    cudaStream_t st, int64_t B) {
   if (n <= 0) return cudaSuccess;
   const int sample_tiles = (n + kTN - 1) / kTN;
-  if (!zero_u) {
+  if (zero_u) {  // first Newton step: no convective part, the affine sums alone
+    AffineParams ap{};
+    ap.aff = op.aff;
+    ap.aff_ld = op.row_tiles * kTM;
+    ap.wts = wts;
+    ap.act = act;
+    ap.Qb = Qb;
+    ap.Ql = Ql;
+    ap.ldw = Qb + Ql;
+    ap.n = n;
+    ap.out = out;
+    ap.ldo = ldo;
+    ap.B = B;
+    oz_affine_kernel<<<dim3(unsigned(op.row_tiles), sample_tiles), kTM, 0, st>>>(ap);
+    return cudaGetLastError();
+  }
+  {
     SliceXParams sp{};
     sp.act = act;
     sp.n = n;
@@ -87,8 +103,7 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
   gp.sa = op.sa;
   gp.sb = sb;
   gp.kchunks = op.kchunks;
-  gp.kc_begin = zero_u ? op.kchunks : 0;
-  gp.no_acc = zero_u ? 1 : 0;
+  gp.kc_begin = 0;
   gp.row_tiles = int(op.row_tiles);
   gp.n = n;
   gp.out = out;

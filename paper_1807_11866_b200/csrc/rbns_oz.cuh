@@ -20,7 +20,7 @@
 //
 // The affine columns (X = [ν]θ_a, S = A_a[r]; a handful of columns whose magnitudes differ from the θ ⊗ u blocks by
 // orders of magnitude) stay out of the sliced GEMM: the epilogue adds Σ_a w_a(b)·A_a[r] in binary64.  The u = 0
-// launch of the first Newton step is that epilogue alone.
+// launch of the first Newton step is that sum alone (oz_affine_kernel, bound by the J write).
 //
 // Kernel (one CTA per SM): output tile = 128 S-rows (MMA M) × 64 samples (MMA N) × s accumulator
 // groups = 448 of the 512 TMEM columns.  Both operands are stored in global memory as ready-made shared-memory
@@ -258,6 +258,61 @@ __global__ void oz_slice_X(const SliceXParams p) {
   if (lane == 0) p.sb[i] = s;
 }
 
+// ---- u = 0 launch (first Newton step): Y[i][r] = Σ_a w_a(i)·A_a[r], the affine columns alone -------------------------
+struct AffineParams {
+  const double* aff;   // [Ql][aff_ld]
+  int64_t aff_ld;
+  const double* wts;   // [B][ldw], the affine weights at column Qb
+  const int32_t* act;  // sample ids (NULL = identity)
+  int32_t Qb, Ql, ldw, n;
+  double* out;         // [n][ldo]
+  int64_t ldo;
+  int64_t B;           // checked builds: sample ids < B (0 = n)
+};
+
+// One CTA = 128 rows (one thread per row, its Ql affine entries in registers) × 64 samples (their weights in shared
+// memory); every sample's 128 outputs are one contiguous 1 KB store of the CTA.  Bound by the J write.
+__global__ void __launch_bounds__(kTM) oz_affine_kernel(const AffineParams p) {
+  __shared__ double wS[kMaxAff * kTN];
+  const int64_t r = int64_t(blockIdx.x) * kTM + threadIdx.x;
+  const int i0 = blockIdx.y * kTN;
+  for (int idx = threadIdx.x; idx < kTN * p.Ql; idx += kTM) {
+    const int a = idx / kTN, c = idx % kTN;
+    const int i = i0 + c;
+    double v = 0.0;
+    if (i < p.n) {
+      const int id = p.act ? p.act[i] : i;
+      RBNS_CHECK(id >= 0 && id < (p.B > 0 ? p.B : p.n));
+      v = p.wts[int64_t(id) * p.ldw + p.Qb + a];
+    }
+    wS[a * kTN + c] = v;
+  }
+  double aff[kMaxAff];
+#pragma unroll
+  for (int a = 0; a < kMaxAff; ++a) aff[a] = a < p.Ql ? p.aff[int64_t(a) * p.aff_ld + r] : 0.0;
+  __syncthreads();
+  RBNS_CHECK(r < p.ldo && r < p.aff_ld);
+#pragma unroll 1
+  for (int c0 = 0; c0 < kTN; c0 += 8) {
+    double y[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < kMaxAff; ++a) {
+      if (a < p.Ql) {
+        const double* wa = wS + a * kTN + c0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = fma(wa[e], aff[a], y[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int i = i0 + c0 + e;
+      if (i < p.n) p.out[int64_t(i) * p.ldo + r] = y[e];
+    }
+  }
+}
+
 // ---- tcgen05 wrappers ----------------------------------------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -377,7 +432,6 @@ struct GemmParams {
   const double* wts;  // [B][ldw] weights, the affine ones at column Qb
   const int32_t* act; // sample ids (NULL = identity)
   int32_t Qb, Ql, ldw;
-  int32_t no_acc;     // u = 0 launch: no MMAs, the affine part only
   int64_t B;          // samples of the call (sample ids < B; checked builds), 0 = n
 #ifdef RBNS_OZ_PROBE
   long long* trace;   // clock64 stamps of CTA (0,0)
@@ -392,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* sbS = reinterpret_cast<double*>(tslot + 4);  // [kTN] X row scales of the tile's samples (0 on the u = 0 launch)
+  double* sbS = reinterpret_cast<double*>(tslot + 4);  // [kTN] X row scales of the tile's samples
   double* wS = sbS + kTN;                               // [Ql][kTN] affine weights of the tile's samples
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -419,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       const int id = p.act ? p.act[i] : i;
       RBNS_CHECK(id >= 0 && id < (p.B > 0 ? p.B : p.n));
       if (a < 0)
-        v = p.no_acc ? 0.0 : p.sb[i];
+        v = p.sb[i];
       else
         v = p.wts[int64_t(id) * p.ldw + p.Qb + a];
     }
@@ -505,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
           phase ^= 1u;
         }
       }
-      if (leader) mma_commit(tfull);  // accumulators of this tile complete (at once on the u = 0 launch: no MMAs)
+      if (leader) mma_commit(tfull);  // accumulators of this tile complete
       __syncwarp();
       OZ_STAMP(p, leader && blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4, (rt - rt_begin) * 8 + 1);
     }
@@ -519,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       const int64_t r = int64_t(rt) * kTM + q * 32 + lane;
       RBNS_CHECK(r < p.ldo && r < p.aff_ld);
       // this row's scale and affine entries, fetched while the MMAs of the tile run
-      const double sar = p.no_acc ? 0.0 : p.sa[r];
+      const double sar = p.sa[r];
       double aff[kMaxAff];
 #pragma unroll
       for (int a = 0; a < kMaxAff; ++a) aff[a] = a < p.Ql ? p.aff[int64_t(a) * p.aff_ld + r] : 0.0;
