@@ -55,6 +55,12 @@ constexpr int kBImg = kTN * kKC;
 constexpr int kAStage = kS * kAImg;
 constexpr int kBStage = kS * kBImg;
 constexpr int kStageBytes = kAStage + kBStage;
+#ifndef RBNS_OZ_STREAM_J
+#define RBNS_OZ_STREAM_J 0     // 1: J written with streaming (evict-first) stores
+#endif
+#ifndef RBNS_OZ_EPI_BACKOFF
+#define RBNS_OZ_EPI_BACKOFF 0  // ns the epilogue warps sleep between probes of the accumulator barrier (0: spin)
+#endif
 #ifndef RBNS_OZ_EPI_WARPS
 #define RBNS_OZ_EPI_WARPS 8
 #endif
@@ -577,7 +583,11 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
       double aff[kMaxAff];
 #pragma unroll
       for (int a = 0; a < kMaxAff; ++a) aff[a] = a < p.Ql ? p.aff[int64_t(a) * p.aff_ld + r] : 0.0;
+#if RBNS_OZ_EPI_BACKOFF
+      mbar_wait_backoff(tfull, tphase, RBNS_OZ_EPI_BACKOFF);
+#else
       mbar_wait(tfull, tphase);
+#endif
       tphase ^= 1u;
       tc_fence_after();
       [[maybe_unused]] const bool tr = blockIdx.x == 0 && blockIdx.y == 0 && rt - rt_begin < 4 && warp == 2 && lane == 0;
@@ -617,7 +627,11 @@ __global__ void __launch_bounds__(kThreads, 1) oz_gemm_kernel(const GemmParams p
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int i = st * kTN + c0 + e;
+#if RBNS_OZ_STREAM_J
+            if (i < p.n) __stcs(p.out + int64_t(i) * p.ldo + r, y[e]);
+#else
             if (i < p.n) p.out[int64_t(i) * p.ldo + r] = y[e];
+#endif
           }
         }
       }
