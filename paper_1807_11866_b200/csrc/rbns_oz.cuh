@@ -107,21 +107,84 @@ __host__ __device__ __forceinline__ void digits(double vs, int (&d)[kS]) {
   for (int i = 0; i < kS; ++i) d[i] = int((signed char)((t >> (8 * (kS - 1 - i))) & 0xffu));
 }
 
+// Eight entries (one 8-κ item) -> the item's 8 bytes of every slice image: digit i of the entries in the two words
+// of slice i (entry e in byte e).  A 4×4 byte transpose of the high and of the low words of four packed digit
+// strings puts digit i of four entries into one word.
+__device__ __forceinline__ void pack_item(const double (&v)[8], uint32_t (&w)[kS][2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if constexpr (kS == 8) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const unsigned long long t = digits_packed(v[4 * h + e]);
+        hi[e] = uint32_t(t >> 32);
+        lo[e] = uint32_t(t);
+      }
+      const uint32_t h01a = __byte_perm(hi[0], hi[1], 0x5140), h23a = __byte_perm(hi[2], hi[3], 0x5140);
+      const uint32_t h01b = __byte_perm(hi[0], hi[1], 0x7362), h23b = __byte_perm(hi[2], hi[3], 0x7362);
+      const uint32_t l01a = __byte_perm(lo[0], lo[1], 0x5140), l23a = __byte_perm(lo[2], lo[3], 0x5140);
+      const uint32_t l01b = __byte_perm(lo[0], lo[1], 0x7362), l23b = __byte_perm(lo[2], lo[3], 0x7362);
+      w[0][h] = __byte_perm(h01b, h23b, 0x7632);  // byte 3 of the high words: d₀
+      w[1][h] = __byte_perm(h01b, h23b, 0x5410);
+      w[2][h] = __byte_perm(h01a, h23a, 0x7632);
+      w[3][h] = __byte_perm(h01a, h23a, 0x5410);
+      w[4][h] = __byte_perm(l01b, l23b, 0x7632);
+      w[5][h] = __byte_perm(l01b, l23b, 0x5410);
+      w[6][h] = __byte_perm(l01a, l23a, 0x7632);
+      w[kS - 1][h] = __byte_perm(l01a, l23a, 0x5410);
+    } else {
+      uint32_t acc[kS];
+#pragma unroll
+      for (int i = 0; i < kS; ++i) acc[i] = 0u;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int d[kS];
+        digits(v[4 * h + e], d);
+#pragma unroll
+        for (int i = 0; i < kS; ++i) acc[i] |= uint32_t(d[i] & 0xff) << (8 * e);
+      }
+#pragma unroll
+      for (int i = 0; i < kS; ++i) w[i][h] = acc[i];
+    }
+  }
+}
+
 // One warp slices one operand row.  val(κ) returns the (column-equilibrated) entry, 0 beyond the real columns.
-// Writes the row's digits into the tile's images, img = tile base + ((kc·kS + i)·ROWS·32), and returns the
-// row's output scale 2^{E−6} (v = v'·2^{E+1}, d₀ weighs 2⁻⁷): NaN for a non-finite row, 0 for a zero row.
+// Writes the row's digits into the tile's images and returns the row's output scale 2^{E−6} (v = v'·2^{E+1},
+// d₀ weighs 2⁻⁷): NaN for a non-finite row, 0 for a zero row.
 // Layout of a stage (32 κ) of ROWS rows: digit i of (row, 16-byte K chunk c) sits at c·CSTRIDE + i·ISTRIDE + row·16.
+// Work items are 8 κ wide (k32/8 per row, dealt round-robin to the lanes).  Up to kCacheItems items per lane (rows of
+// up to 768 columns) keep their entries in registers between the row-maximum pass and the digit pass; wider rows
+// evaluate val twice.
+constexpr int kCacheItems = 3;
 template <int ROWS, int CSTRIDE, int ISTRIDE, class F>
-__device__ __forceinline__ double slice_row(F val, int k32, uint8_t* tile, int row, int lane, int g0 = 0) {
-  const int groups = k32 >> 4;  // 16-κ groups
+__device__ __forceinline__ double slice_row(F val, int k32, uint8_t* tile, int row, int lane) {
+  const int items = k32 >> 3;
+  const bool cached = items <= 32 * kCacheItems;  // warp-uniform
+  double cache[kCacheItems][8];
   double m = 0.0;
   bool bad = false;
-  for (int gi = g0 + lane; gi < groups; gi += 32) {
-#pragma unroll 4
-    for (int e = 0; e < 16; ++e) {
-      const double v = val(gi * 16 + e);
-      bad |= !(fabs(v) <= 1.7976931348623157e308);
-      m = fmax(m, fabs(v));
+  if (cached) {
+#pragma unroll
+    for (int it = 0; it < kCacheItems; ++it) {
+      const int item = lane + 32 * it;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double v = item < items ? val(item * 8 + e) : 0.0;
+        cache[it][e] = v;
+        bad |= !(fabs(v) <= 1.7976931348623157e308);
+        m = fmax(m, fabs(v));
+      }
+    }
+  } else {
+    for (int item = lane; item < items; item += 32) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double v = val(item * 8 + e);
+        bad |= !(fabs(v) <= 1.7976931348623157e308);
+        m = fmax(m, fabs(v));
+      }
     }
   }
 #pragma unroll
@@ -130,59 +193,37 @@ __device__ __forceinline__ double slice_row(F val, int k32, uint8_t* tile, int r
     bad |= __shfl_xor_sync(0xffffffffu, int(bad), o) != 0;
   }
   int E = 0;
-  double down = 0.0;
+  double down = 0.0;  // 0 for a zero or non-finite row: every digit 0
   if (!bad && m > 0.0) {
     E = min(max(ilogb(m) + 1, -900), 900);  // 2^{E−1} ≤ m < 2^E
     down = pow2(-(E + 1));
   }
-  for (int gi = g0 + lane; gi < groups; gi += 32) {
-    uint32_t w[kS][4];
+  auto store = [&](int item, const double (&v)[8]) {
+    uint32_t w[kS][2];
+    pack_item(v, w);
+    const int kc = item >> 2, c = (item >> 1) & 1, half = item & 1;
+    uint8_t* base = tile + size_t(kc) * kS * (ROWS * 32) + c * CSTRIDE + row * 16 + half * 8;
 #pragma unroll
-    for (int e4 = 0; e4 < 4; ++e4) {
-      if constexpr (kS == 8) {
-        // four entries -> eight packed digit strings; a 4×4 byte transpose of the high and of the low words puts
-        // digit i of the four entries into one word of slice i (entry e in byte e)
-        uint32_t hi[4], lo[4];
+    for (int i = 0; i < kS; ++i) *reinterpret_cast<uint2*>(base + size_t(i) * ISTRIDE) = make_uint2(w[i][0], w[i][1]);
+  };
+  if (cached) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double v = (bad || m == 0.0) ? 0.0 : val(gi * 16 + e4 * 4 + e) * down;
-          const unsigned long long t = digits_packed(v);
-          hi[e] = uint32_t(t >> 32);
-          lo[e] = uint32_t(t);
-        }
-        const uint32_t h01a = __byte_perm(hi[0], hi[1], 0x5140), h23a = __byte_perm(hi[2], hi[3], 0x5140);
-        const uint32_t h01b = __byte_perm(hi[0], hi[1], 0x7362), h23b = __byte_perm(hi[2], hi[3], 0x7362);
-        const uint32_t l01a = __byte_perm(lo[0], lo[1], 0x5140), l23a = __byte_perm(lo[2], lo[3], 0x5140);
-        const uint32_t l01b = __byte_perm(lo[0], lo[1], 0x7362), l23b = __byte_perm(lo[2], lo[3], 0x7362);
-        w[0][e4] = __byte_perm(h01b, h23b, 0x7632);  // byte 3 of the high words: d₀
-        w[1][e4] = __byte_perm(h01b, h23b, 0x5410);
-        w[2][e4] = __byte_perm(h01a, h23a, 0x7632);
-        w[3][e4] = __byte_perm(h01a, h23a, 0x5410);
-        w[4][e4] = __byte_perm(l01b, l23b, 0x7632);
-        w[5][e4] = __byte_perm(l01b, l23b, 0x5410);
-        w[6][e4] = __byte_perm(l01a, l23a, 0x7632);
-        w[kS - 1][e4] = __byte_perm(l01a, l23a, 0x5410);
-      } else {
-        uint32_t acc[kS];
+    for (int it = 0; it < kCacheItems; ++it) {
+      const int item = lane + 32 * it;
+      if (item < items) {
+        double v[8];
 #pragma unroll
-        for (int i = 0; i < kS; ++i) acc[i] = 0u;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          int d[kS];
-          const double v = (bad || m == 0.0) ? 0.0 : val(gi * 16 + e4 * 4 + e) * down;
-          digits(v, d);
-#pragma unroll
-          for (int i = 0; i < kS; ++i) acc[i] |= uint32_t(d[i] & 0xff) << (8 * e);
-        }
-#pragma unroll
-        for (int i = 0; i < kS; ++i) w[i][e4] = acc[i];
+        for (int e = 0; e < 8; ++e) v[e] = down == 0.0 ? 0.0 : cache[it][e] * down;
+        store(item, v);
       }
     }
-    const int kc = gi >> 1, c = gi & 1;
-    uint8_t* base = tile + size_t(kc) * kS * (ROWS * 32) + c * CSTRIDE + row * 16;
+  } else {
+    for (int item = lane; item < items; item += 32) {
+      double v[8];
 #pragma unroll
-    for (int i = 0; i < kS; ++i)
-      *reinterpret_cast<uint4*>(base + size_t(i) * ISTRIDE) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+      for (int e = 0; e < 8; ++e) v[e] = down == 0.0 ? 0.0 : val(item * 8 + e) * down;
+      store(item, v);
+    }
   }
   if (bad) return __longlong_as_double(0x7ff8000000000000ll);
   if (m == 0.0) return 0.0;
