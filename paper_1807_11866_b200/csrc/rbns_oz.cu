@@ -77,7 +77,7 @@ cudaError_t launch(const OperandI8& op, const int32_t* act, int n, const double*
     ap.out = out;
     ap.ldo = ldo;
     ap.B = B;
-    oz_affine_kernel<<<dim3(unsigned(op.row_tiles), sample_tiles), kTM, 0, st>>>(ap);
+    oz_affine_kernel<<<dim3(sample_tiles, unsigned(op.row_tiles)), kTM, 0, st>>>(ap);
     return cudaGetLastError();
   }
   {

@@ -324,8 +324,8 @@ struct AffineParams {
 // memory); every sample's 128 outputs are one contiguous 1 KB store of the CTA.  Bound by the J write.
 __global__ void __launch_bounds__(kTM) oz_affine_kernel(const AffineParams p) {
   __shared__ double wS[kMaxAff * kTN];
-  const int64_t r = int64_t(blockIdx.x) * kTM + threadIdx.x;
-  const int i0 = blockIdx.y * kTN;
+  const int64_t r = int64_t(blockIdx.y) * kTM + threadIdx.x;  // row tiles in y (few), sample tiles in x (many)
+  const int i0 = blockIdx.x * kTN;
   for (int idx = threadIdx.x; idx < kTN * p.Ql; idx += kTM) {
     const int a = idx / kTN, c = idx % kTN;
     const int i = i0 + c;
